@@ -167,6 +167,7 @@ typedef struct exd_kernel_stats {
   int64_t select_launches;   /* fused accumulate+select launches timed */
   double select_ms;          /* summed CUDA-event time of those launches */
   int64_t steps;
+  int64_t kernel_launches;   /* every kernel this library launched (all steps) */
 } exd_kernel_stats;
 
 /* ---- status ---------------------------------------------------------- */

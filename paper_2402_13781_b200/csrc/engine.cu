@@ -1,0 +1,889 @@
+// engine.cu — host side of the B200 ExDyna path: the sparsim::Engine
+// replacement (engine.hpp:61-105) and the C ABI of include/exdyna.h.
+//
+// Two deployment shapes share every kernel:
+//   * in-process workers (exd_engine_create): all n workers of the reference's
+//     simulator on one GPU, one stream; collectives are device kernels over
+//     the workers' buffers. No host synchronisation inside a step.
+//   * one rank per GPU (exd_engine_create_rank): the data-parallel job the
+//     paper runs. Collectives are NCCL over NVLink 5 / NVSwitch; the only host
+//     wait per step is the 16 B x n count all-gather that sizes the padded
+//     index all-gather (SURVEY.md §7 hard part 3).
+// Control state (topology, delta, k_t, plan) lives on the device and is
+// advanced by the kernels' single-thread epilogue.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "control.cuh"
+#include "exdyna.h"
+#include "internal.cuh"
+
+using namespace exd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return set_err(EXD_ECUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---- validate(), config.cpp:28-51 -----------------------------------------
+int validate_cfg(const exd_config* in, exd_config* out) {
+  const exd_config c = *in;
+  auto bad = [](const char* m) { return set_err(EXD_EINVAL, m); };
+  if (c.n < 1) return bad("worker count out of range");
+  if (c.n_g < 1) return bad("gradient count out of range");
+  if (c.n_b < 1) return bad("block count out of range");
+  if (!(c.d > 0.0) || c.d > 1.0) return bad("density out of range");
+  if (c.has_delta0 && !(c.delta0 > 0.0)) return bad("delta0 out of range");
+  if (!(c.alpha > 1.0)) return bad("alpha out of range");
+  if (!(c.beta > 1.0)) return bad("beta out of range");
+  if (!(c.gamma > 0.0) || !(c.gamma < 1.0)) return bad("gamma out of range");
+  if (c.blk_move < 1) return bad("blk_move out of range");
+  if (c.min_blk < 1) return bad("min_blk out of range");
+  if (!(c.eta > 0.0)) return bad("eta out of range");
+  if (c.has_max_density_cap && (!(c.max_density_cap > 0.0) || c.max_density_cap > 1.0))
+    return bad("max_density_cap out of range");
+  *out = c;
+  out->k = (int64_t)std::llround(c.d * (double)c.n_g);
+  if (c.n_b < (int64_t)c.n * c.min_blk) return bad("n_b < n*min_blk");
+  if (c.n_b > c.n_g) return bad("n_b > n_g");
+  if (out->k < c.n) return bad("k < n");
+  return EXD_OK;
+}
+
+// ---- build_topology, partition.cpp:22-58 ------------------------------------
+int build_topo(int64_t n_g, int64_t n_b, int n, int64_t min_blk, exd_topology* out,
+               std::string* warning) {
+  if (n < 1 || n > EXD_MAX_WORKERS) return set_err(EXD_EINVAL, "worker count out of range");
+  if (n_b < 1 || n_b > n_g) return set_err(EXD_EINVAL, "n_b out of range");
+  const int64_t q = n_g / n_b;
+  int64_t sz;
+  if (q >= 32) {
+    sz = q - q % 32;
+  } else {
+    sz = q > 1 ? q : 1;
+    if (warning)
+      *warning = "block size " + std::to_string(sz) +
+                 " below 32-element alignment; using unaligned blocks";
+  }
+  const int64_t quo = n_b / n, rem = n_b % n;
+  if (quo < min_blk) return set_err(EXD_EINVAL, "partition would hold fewer than min_blk blocks");
+  std::memset(out, 0, sizeof(*out));
+  out->n = n;
+  out->sz_blk = sz;
+  for (int i = 0; i < n; ++i) out->blk_part[i] = quo + (i < rem ? 1 : 0);
+  for (int i = 1; i < n; ++i) out->blk_pos[i] = out->blk_pos[i - 1] + out->blk_part[i - 1];
+  return EXD_OK;
+}
+
+// ---- NCCL, loaded on first use so the library has no link-time NCCL -------
+struct Nccl {
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      n.why = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return;
+    }
+#define SYM(name) n.name = reinterpret_cast<decltype(n.name)>(dlsym(h, "nccl" #name))
+    SYM(GetUniqueId);
+    SYM(CommInitRank);
+    SYM(CommDestroy);
+    SYM(AllGather);
+    SYM(AllReduce);
+    SYM(Broadcast);
+    SYM(GetErrorString);
+#undef SYM
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllGather && n.AllReduce &&
+           n.Broadcast && n.GetErrorString;
+    if (!n.ok) n.why = "libnccl.so.2 lacks a required symbol";
+  });
+  return n;
+}
+
+#define NC(expr)                                                                        \
+  do {                                                                                  \
+    ncclResult_t _r = (expr);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      return set_err(EXD_ENCCL, std::string(#expr " failed: ") + nccl().GetErrorString(_r)); \
+  } while (0)
+
+// IEEE round-toward-+inf of a positive double to float (the host twin of
+// __double2float_ru): (double)|acc| >= delta  <=>  |acc| >= round_up(delta).
+float round_up_float(double d) {
+  float f = (float)d;
+  if ((double)f < d) f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+size_t elem_size(int dtype) { return dtype == EXD_F64 ? 8 : 4; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct Worker {
+  int rank = 0;
+  RunConst rc{};
+  void* x = nullptr;
+  void* e = nullptr;
+  int32_t* idx = nullptr;
+  void* val = nullptr;
+  int32_t* blk = nullptr;             // 2 x n_b (double-buffered by step parity)
+  unsigned long long* status = nullptr;
+  double* tile_norm = nullptr;
+  Ctrl* ctrl = nullptr;
+  CountRec* cnt = nullptr;            // this worker's count slot
+  int32_t* idx_global = nullptr;
+  void* contrib = nullptr;
+  void* grad_stage = nullptr;         // exd_engine_step_host staging
+  exd_record* rec_host = nullptr;     // mapped pinned
+  exd_record* rec_dev = nullptr;
+  Plan plan0{};                       // host copy of the t = 0 plan
+};
+
+struct exd_engine {
+  exd_config cfg{};
+  exd_options opt{};
+  bool dist = false;
+  int device = 0;
+  int n = 1;
+  cudaStream_t stream = nullptr;
+  std::vector<Worker> w;
+  size_t esz = 4;
+  int64_t tiles = 0;
+  int tile = 0;
+  int64_t cap_part = 0;
+  long long t = 0;                    // steps enqueued
+  // shared device buffers
+  CountRec* counts_all = nullptr;     // [n]
+  CountRec* counts_host = nullptr;    // pinned (dist)
+  void* sum = nullptr;                // all-reduced values [n_g]
+  const int32_t** d_lists = nullptr;  // [n] (sim)
+  const void** d_contribs = nullptr;  // [n] (sim)
+  Ctrl** d_ctrls = nullptr;           // [n local]
+  void* qscratch = nullptr;
+  void* qbits = nullptr;              // quantile result (T)
+  uint32_t* verify_flag = nullptr;    // mapped pinned
+  uint32_t* verify_flag_dev = nullptr;
+  int64_t verify_t = -1;
+  // dist
+  ncclComm_t comm = nullptr;
+  int32_t* recv = nullptr;
+  int64_t recv_cap = 0;
+  // profiling
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, free_ev;
+  exd_kernel_stats stats{};
+  bool has_record = false;
+};
+
+namespace {
+
+int alloc_zero(void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CU(cudaMalloc(p, bytes));
+  CU(cudaMemset(*p, 0, bytes));
+  return EXD_OK;
+}
+
+// The plan of step t = 0 on the host (identical to make_plan on the device):
+// the t = 0 select-only launch needs its tile range before the kernel runs.
+Plan host_plan(const exd_topology& topo0, const int64_t* k_t, const exd_config& c,
+               int static_partitions, int rank) {
+  Plan p{};
+  p.topo = topo0;
+  if (!static_partitions) {
+    int64_t kp[EXD_MAX_WORKERS];
+    rotate(k_t, 0, c.n, kp);
+    adjust(p.topo, kp, c.alpha, c.blk_move, c.min_blk, c.n_g, &p.moves, &p.skips);
+  }
+  p.partition = allocate(p.topo, 0, rank, c.n_g, &p.st, &p.end);
+  return p;
+}
+
+int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int first_rank,
+          int n_local) {
+  exd_config cfg;
+  if (int rc = validate_cfg(raw, &cfg)) return rc;
+  if (cfg.n > EXD_MAX_WORKERS) return set_err(EXD_EINVAL, "worker count out of range");
+  if (cfg.n_g > 0x7fffffffLL) return set_err(EXD_EINVAL, "gradient count exceeds int32 index range");
+  if (opt->sparsifier != EXD_SPARSIFIER_EXDYNA)
+    return set_err(EXD_EUNSUPPORTED, "only the ExDyna sparsifier is on the B200 path");
+  if (cfg.has_max_density_cap)
+    return set_err(EXD_EUNSUPPORTED, "max_density_cap is not implemented on the B200 path");
+  if (opt->dtype != EXD_F32 && opt->dtype != EXD_F64) return set_err(EXD_EINVAL, "dtype out of range");
+  h->cfg = cfg;
+  h->opt = *opt;
+  h->n = cfg.n;
+  h->esz = elem_size(opt->dtype);
+  h->tiles = num_tiles(cfg.n_g, opt->dtype);
+  h->tile = tile_elems(opt->dtype);
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+
+  exd_topology topo0;
+  std::string warn;
+  if (int rc = build_topo(cfg.n_g, cfg.n_b, cfg.n, cfg.min_blk, &topo0, &warn)) return rc;
+  // Largest partition any plan can produce: every other partition keeps at
+  // least min_blk blocks of sz_blk elements.
+  h->cap_part = cfg.n_g - (int64_t)(cfg.n - 1) * cfg.min_blk * topo0.sz_blk;
+  if (h->cap_part < 1) h->cap_part = cfg.n_g;
+
+  const int n = cfg.n;
+  const size_t ng = (size_t)cfg.n_g;
+  h->w.resize(n_local);
+  if (int rc = alloc_zero((void**)&h->counts_all, sizeof(CountRec) * n)) return rc;
+  CU(cudaHostAlloc((void**)&h->counts_host, sizeof(CountRec) * n, cudaHostAllocDefault));
+  if (n > 1) {
+    if (int rc = alloc_zero(&h->sum, h->esz * ng)) return rc;
+  }
+  if (int rc = alloc_zero(&h->qscratch, quantile_scratch_bytes())) return rc;
+  if (int rc = alloc_zero(&h->qbits, 16)) return rc;
+  CU(cudaHostAlloc((void**)&h->verify_flag, sizeof(uint32_t), cudaHostAllocMapped));
+  *h->verify_flag = 0;
+  CU(cudaHostGetDevicePointer((void**)&h->verify_flag_dev, h->verify_flag, 0));
+
+  std::vector<Ctrl*> ctrls;
+  for (int i = 0; i < n_local; ++i) {
+    Worker& wk = h->w[i];
+    wk.rank = first_rank + i;
+    RunConst& rc = wk.rc;
+    rc.n_g = cfg.n_g;
+    rc.n_b = cfg.n_b;
+    rc.k = cfg.k;
+    rc.n = n;
+    rc.rank = wk.rank;
+    rc.eta = cfg.eta;
+    rc.alpha = cfg.alpha;
+    rc.beta = cfg.beta;
+    rc.gamma = cfg.gamma;
+    rc.blk_move = cfg.blk_move;
+    rc.min_blk = cfg.min_blk;
+    rc.static_partitions = opt->static_partitions;
+    rc.dtype = opt->dtype;
+    if (int r = alloc_zero(&wk.x, h->esz * ng)) return r;
+    if (int r = alloc_zero(&wk.e, h->esz * ng)) return r;
+    if (int r = alloc_zero((void**)&wk.idx, 4 * (size_t)h->cap_part)) return r;
+    if (int r = alloc_zero(&wk.val, h->esz * (size_t)h->cap_part)) return r;
+    if (int r = alloc_zero((void**)&wk.blk, 4 * 2 * (size_t)cfg.n_b)) return r;
+    if (int r = alloc_zero((void**)&wk.status, 8 * (size_t)(h->tiles + 1))) return r;
+    if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
+    if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
+    if (n > 1) {
+      if (int r = alloc_zero((void**)&wk.idx_global, 4 * ng)) return r;
+      if (int r = alloc_zero(&wk.contrib, h->esz * ng)) return r;
+    }
+    if (h->dist) {
+      if (int r = alloc_zero((void**)&wk.cnt, sizeof(CountRec))) return r;
+    } else {
+      wk.cnt = h->counts_all + wk.rank;
+    }
+    CU(cudaHostAlloc((void**)&wk.rec_host, sizeof(exd_record), cudaHostAllocMapped));
+    std::memset(wk.rec_host, 0, sizeof(exd_record));
+    CU(cudaHostGetDevicePointer((void**)&wk.rec_dev, wk.rec_host, 0));
+
+    // engine.cpp:68-87: x = 0, e = 0, topology, k_t = k/n, delta = delta0
+    Ctrl c;
+    std::memset(&c, 0, sizeof(c));
+    c.t = 0;
+    c.delta = cfg.has_delta0 ? cfg.delta0 : 0.0;
+    c.has_delta = cfg.has_delta0;
+    c.thr_f = cfg.has_delta0 ? round_up_float(cfg.delta0) : 0.0f;
+    for (int r = 0; r < n; ++r) c.k_t[r] = cfg.k / n;
+    c.topo = topo0;
+    c.epoch = 1;
+    wk.plan0 = host_plan(topo0, c.k_t, cfg, opt->static_partitions, wk.rank);
+    c.plan = wk.plan0;
+    c.last = wk.plan0;
+    CU(cudaMemcpy(wk.ctrl, &c, sizeof(c), cudaMemcpyHostToDevice));
+    ctrls.push_back(wk.ctrl);
+  }
+  CU(cudaMalloc((void**)&h->d_ctrls, sizeof(Ctrl*) * n_local));
+  CU(cudaMemcpy(h->d_ctrls, ctrls.data(), sizeof(Ctrl*) * n_local, cudaMemcpyHostToDevice));
+  if (!h->dist && n > 1) {
+    std::vector<const int32_t*> lists(n);
+    std::vector<const void*> contribs(n);
+    for (int i = 0; i < n; ++i) {
+      lists[i] = h->w[i].idx;
+      contribs[i] = h->w[i].contrib;
+    }
+    CU(cudaMalloc((void**)&h->d_lists, sizeof(void*) * n));
+    CU(cudaMemcpy(h->d_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    CU(cudaMalloc((void**)&h->d_contribs, sizeof(void*) * n));
+    CU(cudaMemcpy(h->d_contribs, contribs.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+  }
+  CU(cudaDeviceSynchronize());
+  return EXD_OK;
+}
+
+void teardown(exd_engine* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& wk : h->w) {
+    cudaFree(wk.x);
+    cudaFree(wk.e);
+    cudaFree(wk.idx);
+    cudaFree(wk.val);
+    cudaFree(wk.blk);
+    cudaFree(wk.status);
+    cudaFree(wk.tile_norm);
+    cudaFree(wk.ctrl);
+    cudaFree(wk.idx_global);
+    cudaFree(wk.contrib);
+    cudaFree(wk.grad_stage);
+    if (h->dist) cudaFree(wk.cnt);
+    cudaFreeHost(wk.rec_host);
+  }
+  cudaFree(h->counts_all);
+  cudaFreeHost(h->counts_host);
+  cudaFree(h->sum);
+  cudaFree(h->d_lists);
+  cudaFree(h->d_contribs);
+  cudaFree(h->d_ctrls);
+  cudaFree(h->qscratch);
+  cudaFree(h->qbits);
+  cudaFree(h->recv);
+  cudaFreeHost(h->verify_flag);
+  for (auto& p : h->pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  for (auto& p : h->free_ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  if (h->comm) nccl().CommDestroy(h->comm);
+  if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+int timed_select(exd_engine* h, int mode, const SelectArgs& a, const RunConst& rc) {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (h->opt.profile_kernels) {
+    if (h->free_ev.empty()) {
+      CU(cudaEventCreate(&ev.first));
+      CU(cudaEventCreate(&ev.second));
+    } else {
+      ev = h->free_ev.back();
+      h->free_ev.pop_back();
+    }
+    CU(cudaEventRecord(ev.first, h->stream));
+  }
+  CU(launch_select(mode, a, rc, h->stream));
+  h->stats.kernel_launches += 1;
+  if (h->opt.profile_kernels) {
+    CU(cudaEventRecord(ev.second, h->stream));
+    h->pending.push_back(ev);
+  }
+  return EXD_OK;
+}
+
+SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
+  SelectArgs a{};
+  a.g = grad;
+  a.e = wk.e;
+  a.x = wk.x;
+  a.idx = wk.idx;
+  a.val = wk.val;
+  a.blk_counts = wk.blk + (h->t & 1) * h->cfg.n_b;
+  a.status = wk.status;
+  a.tile_norm = wk.tile_norm;
+  a.ctrl = wk.ctrl;
+  a.cnt_out = wk.cnt;
+  a.rec = wk.rec_dev;
+  a.tile_base = 0;
+  a.num_tiles = (int32_t)h->tiles;
+  return a;
+}
+
+// Engine::step, engine.cpp:274-350, enqueued on the engine's stream.
+int enqueue_step(exd_engine* h, const void* const* grads) {
+  const exd_config& c = h->cfg;
+  const int n = h->n;
+  const int nl = (int)h->w.size();
+  for (int i = 0; i < nl; ++i)
+    if (!grads || !grads[i]) return set_err(EXD_EINVAL, "null gradient pointer");
+  CU(cudaSetDevice(h->device));
+  // zero the other parity's block counters for the next step
+  for (auto& wk : h->w)
+    CU(cudaMemsetAsync(wk.blk + ((h->t + 1) & 1) * c.n_b, 0, 4 * (size_t)c.n_b, h->stream));
+
+  if (h->t == 0 && !c.has_delta0) {
+    // accumulate_phase, then initialize_threshold (engine.cpp:146-161) on
+    // rank 0's accumulated vector, broadcast, then the selection
+    for (int i = 0; i < nl; ++i) {
+      SelectArgs a = select_args(h, h->w[i], grads[i]);
+      if (int r = timed_select(h, kAccumulate, a, h->w[i].rc)) return r;
+    }
+    const int64_t m = c.n_g;
+    int64_t pos = (int64_t)std::floor((1.0 - c.d) * (double)m);
+    if (pos > m - 1) pos = m - 1;
+    if (!h->dist || h->w[0].rank == 0)
+    {
+      CU(launch_quantile(h->w[0].e, m, pos, h->opt.dtype, h->qscratch, h->qbits, h->stream));
+      h->stats.kernel_launches += 2 + 2 * (int64_t)(8 * h->esz / 8);
+    }
+    if (h->dist && n > 1)
+      NC(nccl().Broadcast(h->qbits, h->qbits, h->esz, ncclUint8, 0, h->comm, h->stream));
+    CU(launch_set_delta(h->d_ctrls, nl, h->qbits, h->opt.dtype, h->stream));
+    h->stats.kernel_launches += 1;
+    for (int i = 0; i < nl; ++i) {
+      Worker& wk = h->w[i];
+      SelectArgs a = select_args(h, wk, grads[i]);
+      const int64_t first = wk.plan0.st / h->tile;
+      const int64_t last = (wk.plan0.end - 1) / h->tile;
+      a.tile_base = (int32_t)first;
+      a.num_tiles = (int32_t)(last - first + 1);
+      if (int r = timed_select(h, kSelectOnly, a, wk.rc)) return r;
+    }
+  } else {
+    for (int i = 0; i < nl; ++i) {
+      SelectArgs a = select_args(h, h->w[i], grads[i]);
+      if (int r = timed_select(h, kFused, a, h->w[i].rc)) return r;
+    }
+  }
+
+  if (n > 1) {
+    if (h->dist) {
+      Worker& wk = h->w[0];
+      NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));
+      CU(cudaMemcpyAsync(h->counts_host, h->counts_all, sizeof(CountRec) * n,
+                         cudaMemcpyDeviceToHost, h->stream));
+      CU(cudaStreamSynchronize(h->stream));
+      int64_t m_t = 0, kp = 0;
+      for (int r = 0; r < n; ++r) {
+        m_t = h->counts_host[r].k > m_t ? h->counts_host[r].k : m_t;
+        kp += h->counts_host[r].k;
+      }
+      if (m_t * n > h->recv_cap) {
+        cudaFree(h->recv);
+        h->recv_cap = m_t * n + (m_t * n) / 4 + 1024;
+        CU(cudaMalloc((void**)&h->recv, 4 * (size_t)h->recv_cap));
+      }
+      if (m_t > 0)
+        NC(nccl().AllGather(wk.idx, h->recv, (size_t)m_t, ncclInt32, h->comm, h->stream));
+      UnionArgs u{};
+      u.lists = nullptr;
+      u.padded = h->recv;
+      u.counts = h->counts_all;
+      u.own_val = wk.val;
+      u.e = wk.e;
+      u.idx_global = wk.idx_global;
+      u.contrib = wk.contrib;
+      u.ctrl = wk.ctrl;
+      CU(launch_union(u, wk.rc, h->stream));
+      h->stats.kernel_launches += 1;
+      if (kp > 0)
+        NC(nccl().AllReduce(wk.contrib, h->sum, (size_t)kp,
+                            h->opt.dtype == EXD_F64 ? ncclFloat64 : ncclFloat32, ncclSum,
+                            h->comm, h->stream));
+      FinalizeArgs f{};
+      f.idx_global = wk.idx_global;
+      f.sum = h->sum;
+      f.x = wk.x;
+      f.ctrl = wk.ctrl;
+      f.counts = h->counts_all;
+      f.rec = wk.rec_dev;
+      CU(launch_finalize(f, wk.rc, h->stream));
+      h->stats.kernel_launches += 1;
+    } else {
+      for (int i = 0; i < nl; ++i) {
+        Worker& wk = h->w[i];
+        UnionArgs u{};
+        u.lists = h->d_lists;
+        u.padded = nullptr;
+        u.counts = h->counts_all;
+        u.own_val = wk.val;
+        u.e = wk.e;
+        u.idx_global = wk.idx_global;
+        u.contrib = wk.contrib;
+        u.ctrl = wk.ctrl;
+        CU(launch_union(u, wk.rc, h->stream));
+        h->stats.kernel_launches += 1;
+      h->stats.kernel_launches += 1;
+      }
+      CU(launch_allreduce_local(h->d_contribs, h->sum, h->w[0].ctrl, h->counts_all, h->w[0].rc,
+                                h->stream));
+      h->stats.kernel_launches += 1;
+      for (int i = 0; i < nl; ++i) {
+        Worker& wk = h->w[i];
+        FinalizeArgs f{};
+        f.idx_global = wk.idx_global;
+        f.sum = h->sum;
+        f.x = wk.x;
+        f.ctrl = wk.ctrl;
+        f.counts = h->counts_all;
+        f.rec = wk.rec_dev;
+        CU(launch_finalize(f, wk.rc, h->stream));
+        h->stats.kernel_launches += 1;
+      h->stats.kernel_launches += 1;
+      }
+    }
+  }
+  // verify_replication, engine.cpp:251-272 (in-process replicas)
+  if (h->opt.verify_replication && !h->dist && nl > 1) {
+    for (int i = 1; i < nl; ++i)
+      CU(launch_verify_replication(h->w[0].ctrl, h->w[i].ctrl, h->w[0].x, h->w[i].x, c.n_g,
+                                   h->opt.dtype, h->w[i].rank, h->verify_flag_dev, h->stream));
+    h->stats.kernel_launches += nl - 1;
+    h->verify_t = h->t;
+  }
+  h->t += 1;
+  h->stats.steps += 1;
+  h->has_record = true;
+  return EXD_OK;
+}
+
+int sync_engine(exd_engine* h, exd_record* out) {
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  for (auto& p : h->pending) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, p.first, p.second));
+    h->stats.select_ms += ms;
+    h->stats.select_launches += 1;
+    h->free_ev.push_back(p);
+  }
+  h->pending.clear();
+  if (*h->verify_flag) {
+    const uint32_t f = *h->verify_flag;
+    const char* field = (f & 1) ? "delta" : (f & 2) ? "k_t" : (f & 4) ? "topology" : "x";
+    char msg[160];
+    std::snprintf(msg, sizeof msg, "replicated state diverged at iteration %lld: rank %u field %s",
+                  (long long)h->verify_t, f >> 8, field);
+    *h->verify_flag = 0;
+    return set_err(EXD_EINVARIANT, msg);
+  }
+  if (out) {
+    if (!h->has_record) std::memset(out, 0, sizeof(*out));
+    else std::memcpy(out, h->w[0].rec_host, sizeof(*out));
+  }
+  return EXD_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* exd_last_error(void) { return g_err.c_str(); }
+int32_t exd_version(void) { return 1; }
+
+int exd_validate(const exd_config* in, exd_config* out) {
+  if (!in || !out) return set_err(EXD_EINVAL, "null argument");
+  return validate_cfg(in, out);
+}
+
+int64_t exd_default_block_count(int32_t n) { return 64 * (int64_t)n; }
+
+int exd_build_topology(int64_t n_g, int64_t n_b, int32_t n, int64_t min_blk, exd_topology* out,
+                       char* warning, size_t warning_len) {
+  std::string w;
+  const int rc = build_topo(n_g, n_b, n, min_blk, out, &w);
+  if (warning && warning_len) {
+    std::strncpy(warning, w.c_str(), warning_len - 1);
+    warning[warning_len - 1] = 0;
+  }
+  return rc;
+}
+
+int exd_partition_range(const exd_topology* topo, int32_t p, int64_t n_g, int64_t* st,
+                        int64_t* end) {
+  if (p < 0 || p >= topo->n) return set_err(EXD_EINVAL, "partition out of range");
+  partition_range(*topo, p, n_g, st, end);
+  return EXD_OK;
+}
+
+int exd_rotate_to_partition_order(const int64_t* k_rank, int64_t t, int32_t n, int64_t* k_part) {
+  if (n < 1 || n > EXD_MAX_WORKERS) return set_err(EXD_EINVAL, "partial-k length mismatch");
+  rotate(k_rank, t, n, k_part);
+  return EXD_OK;
+}
+
+int exd_adjust_topology(exd_topology* topo, int64_t* k_part, double alpha, int64_t blk_move,
+                        int64_t min_blk, int64_t n_g, int32_t* moves, int32_t* skips) {
+  int32_t mv = 0, sk = 0;
+  adjust(*topo, k_part, alpha, blk_move, min_blk, n_g, &mv, &sk);
+  if (moves) *moves = mv;
+  if (skips) *skips = sk;
+  return EXD_OK;
+}
+
+int exd_allocate_partition(const exd_topology* topo, int64_t t, int32_t rank, int64_t n_g,
+                           int32_t* partition, int64_t* st, int64_t* end) {
+  const int p = allocate(*topo, t, rank, n_g, st, end);
+  if (partition) *partition = p;
+  return EXD_OK;
+}
+
+double exd_scale_threshold(int64_t k, int64_t k_prime, double delta, double beta, double gamma) {
+  return scale_threshold(k, k_prime, delta, beta, gamma);
+}
+
+int exd_gather_stats_of(const int64_t* k_rank, int32_t n, exd_gather_stats* out) {
+  if (n < 1 || n > EXD_MAX_WORKERS) return set_err(EXD_EINVAL, "worker count out of range");
+  gather_stats(k_rank, n, out);
+  return EXD_OK;
+}
+
+int exd_initial_threshold_device(const void* mags_dev, int64_t m, int32_t dtype, double d,
+                                 double* out) {
+  if (m < 1) return set_err(EXD_EINVAL, "initial_threshold: empty sample");
+  int64_t pos = (int64_t)std::floor((1.0 - d) * (double)m);
+  if (pos > m - 1) pos = m - 1;
+  void* scratch = nullptr;
+  void* bits = nullptr;
+  CU(cudaMalloc(&scratch, quantile_scratch_bytes()));
+  CU(cudaMalloc(&bits, 16));
+  CU(launch_quantile(mags_dev, m, pos, dtype, scratch, bits, 0));
+  if (dtype == EXD_F64) {
+    CU(cudaMemcpy(out, bits, 8, cudaMemcpyDeviceToHost));
+  } else {
+    float f;
+    CU(cudaMemcpy(&f, bits, 4, cudaMemcpyDeviceToHost));
+    *out = (double)f;
+  }
+  cudaFree(scratch);
+  cudaFree(bits);
+  return EXD_OK;
+}
+
+int exd_synthetic_gradient(const exd_stream_spec* spec, int64_t t, int32_t rank, int32_t dtype,
+                           void* out_dev, void* cuda_stream) {
+  if (!spec || spec->nseg < 1 || spec->nseg > EXD_MAX_SEGMENTS)
+    return set_err(EXD_EINVAL, "stream has no segments");
+  int64_t total = 0;
+  for (int i = 0; i < spec->nseg; ++i) {
+    if (spec->seg_length[i] < 1) return set_err(EXD_EINVAL, "segment length out of range");
+    if (!(spec->seg_scale[i] > 0.0)) return set_err(EXD_EINVAL, "segment scale out of range");
+    total += spec->seg_length[i];
+  }
+  if (total != spec->n_g) return set_err(EXD_EINVAL, "segment lengths do not sum to n_g");
+  CU(launch_synthetic(spec, t, rank, dtype, out_dev, (cudaStream_t)cuda_stream));
+  return EXD_OK;
+}
+
+int exd_engine_create(const exd_config* cfg, const exd_options* opt, const int32_t* devices,
+                      int32_t ndev, exd_engine** out) {
+  if (!cfg || !opt || !out) return set_err(EXD_EINVAL, "null argument");
+  if (ndev > 1 && cfg->n > 1)
+    return set_err(EXD_EUNSUPPORTED,
+                   "in-process workers share one device; use exd_engine_create_rank per GPU");
+  auto* h = new exd_engine;
+  h->dist = false;
+  h->device = (devices && ndev > 0) ? devices[0] : 0;
+  const int rc = setup(h, cfg, opt, 0, cfg->n > 0 ? cfg->n : 1);
+  if (rc) {
+    const std::string msg = g_err;
+    teardown(h);
+    delete h;
+    g_err = msg;
+    return rc;
+  }
+  *out = h;
+  return EXD_OK;
+}
+
+int exd_nccl_unique_id(uint8_t* out) {
+  Nccl& nc = nccl();
+  if (!nc.ok) return set_err(EXD_ENCCL, nc.why);
+  ncclUniqueId id;
+  NC(nc.GetUniqueId(&id));
+  std::memcpy(out, &id, EXD_NCCL_ID_BYTES);
+  return EXD_OK;
+}
+
+int exd_engine_create_rank(const exd_config* cfg, const exd_options* opt, int32_t rank,
+                           int32_t device, const uint8_t* nccl_id, exd_engine** out) {
+  if (!cfg || !opt || !out) return set_err(EXD_EINVAL, "null argument");
+  if (rank < 0 || rank >= cfg->n) return set_err(EXD_EINVAL, "rank out of range");
+  auto* h = new exd_engine;
+  h->dist = true;
+  h->device = device;
+  int rc = setup(h, cfg, opt, rank, 1);
+  if (!rc && cfg->n > 1) {
+    Nccl& nc = nccl();
+    if (!nc.ok) {
+      rc = set_err(EXD_ENCCL, nc.why);
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, EXD_NCCL_ID_BYTES);
+      cudaSetDevice(device);
+      ncclResult_t r = nc.CommInitRank(&h->comm, cfg->n, id, rank);
+      if (r != ncclSuccess) rc = set_err(EXD_ENCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
+    }
+  }
+  if (rc) {
+    const std::string msg = g_err;
+    teardown(h);
+    delete h;
+    g_err = msg;
+    return rc;
+  }
+  *out = h;
+  return EXD_OK;
+}
+
+void exd_engine_destroy(exd_engine* h) {
+  teardown(h);
+  delete h;
+}
+
+int32_t exd_engine_local_workers(const exd_engine* h) { return (int32_t)h->w.size(); }
+int32_t exd_engine_first_rank(const exd_engine* h) { return h->w.empty() ? 0 : h->w[0].rank; }
+int64_t exd_engine_iteration(const exd_engine* h) { return h->t; }
+void* exd_engine_stream(const exd_engine* h, int32_t) { return (void*)h->stream; }
+
+int exd_engine_step_async(exd_engine* h, const void* const* grads_dev) {
+  return enqueue_step(h, grads_dev);
+}
+
+int exd_engine_sync(exd_engine* h, exd_record* out) { return sync_engine(h, out); }
+
+int exd_engine_step(exd_engine* h, const void* const* grads_dev, exd_record* out) {
+  if (int rc = enqueue_step(h, grads_dev)) return rc;
+  return sync_engine(h, out);
+}
+
+int exd_engine_step_host(exd_engine* h, const void* const* grads_host, exd_record* out) {
+  const size_t bytes = h->esz * (size_t)h->cfg.n_g;
+  std::vector<const void*> dev(h->w.size());
+  CU(cudaSetDevice(h->device));
+  for (size_t i = 0; i < h->w.size(); ++i) {
+    Worker& wk = h->w[i];
+    if (!wk.grad_stage) CU(cudaMalloc(&wk.grad_stage, bytes));
+    CU(cudaMemcpyAsync(wk.grad_stage, grads_host[i], bytes, cudaMemcpyHostToDevice, h->stream));
+    dev[i] = wk.grad_stage;
+  }
+  return exd_engine_step(h, dev.data(), out);
+}
+
+int exd_engine_get_state(exd_engine* h, int32_t w, exd_worker_state* out) {
+  if (w < 0 || w >= (int)h->w.size()) return set_err(EXD_EINVAL, "worker out of range");
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  Ctrl c;
+  CU(cudaMemcpy(&c, h->w[w].ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+  std::memset(out, 0, sizeof(*out));
+  out->t = c.t;
+  out->rank = h->w[w].rank;
+  out->delta = c.delta;
+  out->partition = c.last.partition;
+  out->st = c.last.st;
+  out->end = c.last.end;
+  for (int i = 0; i < h->n; ++i) out->k_t[i] = c.k_t[i];
+  out->topology = c.topo;
+  return EXD_OK;
+}
+
+int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host, int64_t cap,
+                        int64_t* len) {
+  if (w < 0 || w >= (int)h->w.size()) return set_err(EXD_EINVAL, "worker out of range");
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  Worker& wk = h->w[w];
+  const exd_record& rec = *h->w[w].rec_host;
+  int64_t n_el = 0;
+  size_t es = h->esz;
+  const void* src = nullptr;
+  switch (which) {
+    case EXD_VEC_X: n_el = h->cfg.n_g; src = wk.x; break;
+    case EXD_VEC_E: n_el = h->cfg.n_g; src = wk.e; break;
+    case EXD_VEC_IDX_GLOBAL:
+      n_el = h->has_record ? rec.k_prime : 0;
+      src = h->n > 1 ? (const void*)wk.idx_global : (const void*)wk.idx;
+      es = 4;
+      break;
+    case EXD_VEC_LOCAL_IDX:
+    case EXD_VEC_LOCAL_VAL: {
+      CountRec cr;
+      CU(cudaMemcpy(&cr, wk.cnt, sizeof(cr), cudaMemcpyDeviceToHost));
+      n_el = h->has_record ? cr.k : 0;
+      src = which == EXD_VEC_LOCAL_IDX ? (const void*)wk.idx : wk.val;
+      if (which == EXD_VEC_LOCAL_IDX) es = 4;
+      break;
+    }
+    case EXD_VEC_BLOCK_COUNTS:
+      n_el = h->cfg.n_b;
+      src = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;  // parity of the last step
+      es = 4;
+      break;
+    case EXD_VEC_SUM:
+      n_el = h->has_record ? rec.k_prime : 0;
+      src = h->n > 1 ? h->sum : wk.val;
+      break;
+    default:
+      return set_err(EXD_EINVAL, "unknown vector");
+  }
+  if (len) *len = n_el;
+  if (!host) return EXD_OK;
+  if (n_el > cap) return set_err(EXD_EINVAL, "host buffer too small");
+  if (n_el) CU(cudaMemcpy(host, src, es * (size_t)n_el, cudaMemcpyDeviceToHost));
+  return EXD_OK;
+}
+
+int exd_engine_copy_in(exd_engine* h, int32_t w, int32_t which, const void* host, int64_t n_el) {
+  if (w < 0 || w >= (int)h->w.size()) return set_err(EXD_EINVAL, "worker out of range");
+  if (which != EXD_VEC_X && which != EXD_VEC_E) return set_err(EXD_EINVAL, "only x and e are writable");
+  if (n_el != h->cfg.n_g) return set_err(EXD_EINVAL, "length != n_g");
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  CU(cudaMemcpy(which == EXD_VEC_X ? h->w[w].x : h->w[w].e, host, h->esz * (size_t)n_el,
+                cudaMemcpyHostToDevice));
+  return EXD_OK;
+}
+
+int exd_engine_kernel_stats(exd_engine* h, exd_kernel_stats* out) {
+  if (int rc = sync_engine(h, nullptr)) return rc;
+  *out = h->stats;
+  return EXD_OK;
+}
+
+int exd_engine_reset_kernel_stats(exd_engine* h) {
+  if (int rc = sync_engine(h, nullptr)) return rc;
+  std::memset(&h->stats, 0, sizeof(h->stats));
+  return EXD_OK;
+}
+
+int exd_flush_l2(int32_t device, void* cuda_stream) {
+  static void* buf[16] = {nullptr};
+  static size_t bytes = 0;
+  if (device < 0 || device >= 16) return set_err(EXD_EINVAL, "device out of range");
+  CU(cudaSetDevice(device));
+  if (!buf[device]) {
+    int l2 = 0;
+    CU(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+    bytes = (size_t)l2 * 2 + (64u << 20);
+    CU(cudaMalloc(&buf[device], bytes));
+  }
+  CU(cudaMemsetAsync(buf[device], device + 1, bytes, (cudaStream_t)cuda_stream));
+  return EXD_OK;
+}
+
+}  // extern "C"

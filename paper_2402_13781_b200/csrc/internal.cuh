@@ -1,0 +1,124 @@
+// internal.cuh — device-resident state and kernel launch interfaces shared by
+// kernels.cu and engine.cu. Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "control.cuh"
+#include "exdyna.h"
+
+namespace exd {
+
+// Per-step plan of one worker: the reference's accumulate-phase control
+// (rotate -> adjust -> allocate, engine.cpp:125-131), computed on the device
+// at the end of the previous step so the fused kernel never waits on the host.
+struct Plan {
+  exd_topology topo;        // topology after this step's adjust
+  int64_t st, end;          // exclusive search range [st, end)
+  int32_t partition;
+  int32_t moves, skips;     // AdjustStats
+  int32_t reserved;
+};
+
+// Replicated control state of one worker (WorkerState minus the vectors,
+// types.hpp:73-80) plus the device-side bookkeeping of the fused kernel.
+struct Ctrl {
+  int64_t t;                // iteration the next step runs
+  double delta;             // selection threshold (fp64, as the reference)
+  float thr_f;              // __double2float_ru(delta): fp32 compare key
+  int32_t has_delta;        // delta known (delta0 given or estimated)
+  int64_t k_t[EXD_MAX_WORKERS];  // last gathered counts, rank order
+  exd_topology topo;        // committed topology (reference's WorkerState::topology)
+  Plan plan;                // plan of step t
+  Plan last;                // plan the last completed step ran with
+  // fused-kernel bookkeeping (self-resetting)
+  uint32_t ticket;          // dynamic tile ticket
+  uint32_t done;            // completed CTAs
+  uint32_t epoch;           // look-back status epoch (never 0)
+  uint32_t error;           // device-detected invariant violation (bitmask)
+  int64_t k_local;          // own selection count of the running step
+  double norm2;             // ||e_entering||^2 of the running step
+};
+
+// What each rank contributes to the count all-gather (16 bytes).
+struct CountRec {
+  int64_t k;
+  double norm2;
+};
+
+// Everything a kernel needs to know about the run (by value).
+struct RunConst {
+  int64_t n_g, n_b, k;
+  int32_t n, rank;
+  double eta, alpha, beta, gamma;
+  int64_t blk_move, min_blk;
+  int32_t static_partitions;
+  int32_t dtype;
+};
+
+struct SelectArgs {
+  const void* g;            // T[n_g]   gradient (ACCUM)
+  void* e;                  // T[n_g]   residual, in place
+  void* x;                  // T[n_g]   model (fused n == 1 only)
+  int32_t* idx;             // [cap]    own selection, ascending
+  void* val;                // T[cap]   own selected values
+  int32_t* blk_counts;      // [n_b]    per-block selection counts
+  unsigned long long* status;  // per scan tile look-back words
+  double* tile_norm;        // per tile ||e||^2 partial
+  Ctrl* ctrl;
+  CountRec* cnt_out;        // this rank's slot of the count all-gather
+  exd_record* rec;          // fused n == 1: record (mapped host memory)
+  int32_t tile_base;        // first tile covered by the launch
+  int32_t num_tiles;        // tiles covered (== gridDim.x)
+};
+
+// union build + contribution gather + residual clear (K4 + K5)
+struct UnionArgs {
+  const int32_t* const* lists;  // [n] per-rank index lists (device); NULL -> padded
+  const int32_t* padded;        // dist mode: all-gather recv buffer, stride m_t
+  const CountRec* counts;       // [n] gathered counts
+  const void* own_val;          // own selected values (T)
+  void* e;                      // T residual, cleared at the union
+  int32_t* idx_global;          // [k'] out
+  void* contrib;                // T [k'] out
+  const Ctrl* ctrl;
+};
+
+struct FinalizeArgs {
+  const int32_t* idx_global;
+  const void* sum;              // T [k'] all-reduced values
+  void* x;
+  Ctrl* ctrl;
+  const CountRec* counts;       // [n]
+  exd_record* rec;              // record (mapped host memory)
+};
+
+// kernel launchers (kernels.cu)
+int tile_elems(int dtype);
+int64_t num_tiles(int64_t n_g, int dtype);
+cudaError_t launch_plan(Ctrl* ctrl, RunConst rc, cudaStream_t s);
+cudaError_t launch_select(int mode, SelectArgs a, RunConst rc, cudaStream_t s);
+cudaError_t launch_union(UnionArgs a, RunConst rc, cudaStream_t s);
+cudaError_t launch_allreduce_local(const void* const* contribs, void* sum, const Ctrl* ctrl,
+                                   const CountRec* counts, RunConst rc, cudaStream_t s);
+cudaError_t launch_finalize(FinalizeArgs a, RunConst rc, cudaStream_t s);
+cudaError_t launch_set_delta(Ctrl* const* ctrls, int nctrl, const void* src_bits, int dtype,
+                             cudaStream_t s);
+cudaError_t launch_quantile(const void* v, int64_t m, int64_t pos, int dtype, void* scratch,
+                            void* out_bits, cudaStream_t s);
+size_t quantile_scratch_bytes();
+cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void* x0,
+                                      const void* xw, int64_t n_g, int dtype, int32_t w,
+                                      uint32_t* flag, cudaStream_t s);
+cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
+                             void* out, cudaStream_t s);
+
+// selection modes of launch_select
+enum SelectMode {
+  kFused = 0,        // accumulate + select + compact (+ x update and finalize when n == 1)
+  kAccumulate = 1,   // t = 0 without delta0: accumulate only
+  kSelectOnly = 2,   // t = 0 without delta0: select over the partition only
+};
+
+}  // namespace exd
