@@ -164,10 +164,12 @@ enum {
 };
 
 typedef struct exd_kernel_stats {
-  int64_t select_launches;   /* fused accumulate+select launches timed */
+  int64_t select_launches;   /* stream-kernel launches timed (accumulate+select+stage) */
   double select_ms;          /* summed CUDA-event time of those launches */
   int64_t steps;
   int64_t kernel_launches;   /* every kernel this library launched (all steps) */
+  int64_t finish_launches;   /* finish-kernel launches timed (offsets, lists, epilogue) */
+  double finish_ms;          /* summed CUDA-event time of those launches */
 } exd_kernel_stats;
 
 /* ---- status ---------------------------------------------------------- */

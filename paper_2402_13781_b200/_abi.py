@@ -85,7 +85,7 @@ class exd_stream_spec(C.Structure):
 
 class exd_kernel_stats(C.Structure):
     _fields_ = [("select_launches", i64), ("select_ms", f64), ("steps", i64),
-                ("kernel_launches", i64)]
+                ("kernel_launches", i64), ("finish_launches", i64), ("finish_ms", f64)]
 
 
 RECORD_FIELDS = ("t", "k_prime", "density", "eps", "m_t", "c_t", "f_t", "global_err",

@@ -160,7 +160,11 @@ struct Worker {
   int32_t* idx = nullptr;
   void* val = nullptr;
   int32_t* blk = nullptr;             // 2 x n_b (double-buffered by step parity)
-  unsigned long long* status = nullptr;
+  int32_t* stage_idx = nullptr;       // warp-chunk staging of the compaction
+  void* stage_val = nullptr;
+  int32_t* chunk_count = nullptr;
+  int32_t* tile_count = nullptr;
+  double* cta_norm = nullptr;
   double* tile_norm = nullptr;
   Ctrl* ctrl = nullptr;
   CountRec* cnt = nullptr;            // this worker's count slot
@@ -202,7 +206,12 @@ struct exd_engine {
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
   // profiling
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, free_ev;
+  struct Pending {
+    cudaEvent_t a, b, c;
+    bool finish;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_ev;
   exd_kernel_stats stats{};
   bool has_record = false;
 };
@@ -296,7 +305,12 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero((void**)&wk.idx, 4 * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero(&wk.val, h->esz * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero((void**)&wk.blk, 4 * 2 * (size_t)cfg.n_b)) return r;
-    if (int r = alloc_zero((void**)&wk.status, 8 * (size_t)(h->tiles + 1))) return r;
+    const size_t stage_cap = (size_t)h->cap_part + 2 * (size_t)h->tile;
+    if (int r = alloc_zero((void**)&wk.stage_idx, 4 * stage_cap)) return r;
+    if (int r = alloc_zero(&wk.stage_val, h->esz * stage_cap)) return r;
+    if (int r = alloc_zero((void**)&wk.chunk_count, 4 * (size_t)(h->tiles + 1) * kChunksPerTile)) return r;
+    if (int r = alloc_zero((void**)&wk.tile_count, 4 * (size_t)(h->tiles + 8))) return r;
+    if (int r = alloc_zero((void**)&wk.cta_norm, 8 * (size_t)kMaxCtas)) return r;
     if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
     if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
     if (n > 1) {
@@ -356,7 +370,11 @@ void teardown(exd_engine* h) {
     cudaFree(wk.idx);
     cudaFree(wk.val);
     cudaFree(wk.blk);
-    cudaFree(wk.status);
+    cudaFree(wk.stage_idx);
+    cudaFree(wk.stage_val);
+    cudaFree(wk.chunk_count);
+    cudaFree(wk.tile_count);
+    cudaFree(wk.cta_norm);
     cudaFree(wk.tile_norm);
     cudaFree(wk.ctrl);
     cudaFree(wk.idx_global);
@@ -375,29 +393,38 @@ void teardown(exd_engine* h) {
   cudaFree(h->qbits);
   cudaFree(h->recv);
   cudaFreeHost(h->verify_flag);
-  for (auto& p : h->pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
-  for (auto& p : h->free_ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  for (auto& p : h->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); cudaEventDestroy(p.c); }
+  for (auto& ev : h->free_ev) cudaEventDestroy(ev);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
-int timed_select(exd_engine* h, int mode, const SelectArgs& a, const RunConst& rc) {
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (h->opt.profile_kernels) {
-    if (h->free_ev.empty()) {
-      CU(cudaEventCreate(&ev.first));
-      CU(cudaEventCreate(&ev.second));
-    } else {
-      ev = h->free_ev.back();
-      h->free_ev.pop_back();
+// K1 (stream) and, unless accumulate-only, K2 (finish); CUDA events around
+// each when profiling so the bench can report the stream kernel's own time.
+int select_phase(exd_engine* h, int mode, const SelectArgs& a, const RunConst& rc) {
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  const bool prof = h->opt.profile_kernels != 0;
+  if (prof) {
+    for (auto& x : ev) {
+      if (h->free_ev.empty()) {
+        CU(cudaEventCreate(&x));
+      } else {
+        x = h->free_ev.back();
+        h->free_ev.pop_back();
+      }
     }
-    CU(cudaEventRecord(ev.first, h->stream));
+    CU(cudaEventRecord(ev[0], h->stream));
   }
-  CU(launch_select(mode, a, rc, h->stream));
+  CU(launch_stream(mode, a, rc, h->stream));
   h->stats.kernel_launches += 1;
-  if (h->opt.profile_kernels) {
-    CU(cudaEventRecord(ev.second, h->stream));
-    h->pending.push_back(ev);
+  if (prof) CU(cudaEventRecord(ev[1], h->stream));
+  if (mode != kAccumulate) {
+    CU(launch_finish(a, rc, h->stream));
+    h->stats.kernel_launches += 1;
+  }
+  if (prof) {
+    CU(cudaEventRecord(ev[2], h->stream));
+    h->pending.push_back({ev[0], ev[1], ev[2], mode != kAccumulate});
   }
   return EXD_OK;
 }
@@ -410,8 +437,12 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.idx = wk.idx;
   a.val = wk.val;
   a.blk_counts = wk.blk + (h->t & 1) * h->cfg.n_b;
-  a.status = wk.status;
+  a.stage_idx = wk.stage_idx;
+  a.stage_val = wk.stage_val;
+  a.chunk_count = wk.chunk_count;
+  a.tile_count = wk.tile_count;
   a.tile_norm = wk.tile_norm;
+  a.cta_norm = wk.cta_norm;
   a.ctrl = wk.ctrl;
   a.cnt_out = wk.cnt;
   a.rec = wk.rec_dev;
@@ -437,7 +468,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
     // rank 0's accumulated vector, broadcast, then the selection
     for (int i = 0; i < nl; ++i) {
       SelectArgs a = select_args(h, h->w[i], grads[i]);
-      if (int r = timed_select(h, kAccumulate, a, h->w[i].rc)) return r;
+      if (int r = select_phase(h, kAccumulate, a, h->w[i].rc)) return r;
     }
     const int64_t m = c.n_g;
     int64_t pos = (int64_t)std::floor((1.0 - c.d) * (double)m);
@@ -458,12 +489,12 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       const int64_t last = (wk.plan0.end - 1) / h->tile;
       a.tile_base = (int32_t)first;
       a.num_tiles = (int32_t)(last - first + 1);
-      if (int r = timed_select(h, kSelectOnly, a, wk.rc)) return r;
+      if (int r = select_phase(h, kSelectOnly, a, wk.rc)) return r;
     }
   } else {
     for (int i = 0; i < nl; ++i) {
       SelectArgs a = select_args(h, h->w[i], grads[i]);
-      if (int r = timed_select(h, kFused, a, h->w[i].rc)) return r;
+      if (int r = select_phase(h, kFused, a, h->w[i].rc)) return r;
     }
   }
 
@@ -563,10 +594,17 @@ int sync_engine(exd_engine* h, exd_record* out) {
   CU(cudaStreamSynchronize(h->stream));
   for (auto& p : h->pending) {
     float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, p.first, p.second));
+    CU(cudaEventElapsedTime(&ms, p.a, p.b));
     h->stats.select_ms += ms;
     h->stats.select_launches += 1;
-    h->free_ev.push_back(p);
+    if (p.finish) {
+      CU(cudaEventElapsedTime(&ms, p.b, p.c));
+      h->stats.finish_ms += ms;
+      h->stats.finish_launches += 1;
+    }
+    h->free_ev.push_back(p.a);
+    h->free_ev.push_back(p.b);
+    h->free_ev.push_back(p.c);
   }
   h->pending.clear();
   if (*h->verify_flag) {
@@ -882,7 +920,7 @@ int exd_flush_l2(int32_t device, void* cuda_stream) {
     bytes = (size_t)l2 * 2 + (64u << 20);
     CU(cudaMalloc(&buf[device], bytes));
   }
-  CU(cudaMemsetAsync(buf[device], device + 1, bytes, (cudaStream_t)cuda_stream));
+  CU(launch_l2_flush(buf[device], bytes, (cudaStream_t)cuda_stream));
   return EXD_OK;
 }
 

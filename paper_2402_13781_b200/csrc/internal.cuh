@@ -64,14 +64,21 @@ struct SelectArgs {
   int32_t* idx;             // [cap]    own selection, ascending
   void* val;                // T[cap]   own selected values
   int32_t* blk_counts;      // [n_b]    per-block selection counts
-  unsigned long long* status;  // per scan tile look-back words
-  double* tile_norm;        // per tile ||e||^2 partial
+  int32_t* stage_idx;       // [cap + 2 tiles] warp-chunk staging of the compaction
+  void* stage_val;          // T[...]
+  int32_t* chunk_count;     // [tiles * kChunksPerTile] selected per warp chunk
+  int32_t* tile_count;      // [tiles + 4] selected per tile (<= tile size)
+  double* tile_norm;        // [tiles] ||e_entering||^2 partial per tile
+  double* cta_norm;         // [kMaxCtas] finish-kernel partials
   Ctrl* ctrl;
   CountRec* cnt_out;        // this rank's slot of the count all-gather
   exd_record* rec;          // fused n == 1: record (mapped host memory)
-  int32_t tile_base;        // first tile covered by the launch
-  int32_t num_tiles;        // tiles covered (== gridDim.x)
+  int32_t tile_base;        // first tile covered by the stream launch
+  int32_t num_tiles;        // tiles covered by the stream launch
 };
+
+constexpr int kMaxCtas = 2048;
+constexpr int kChunksPerTile = 8;  // one warp chunk per warp of the stream kernel
 
 // union build + contribution gather + residual clear (K4 + K5)
 struct UnionArgs {
@@ -98,7 +105,8 @@ struct FinalizeArgs {
 int tile_elems(int dtype);
 int64_t num_tiles(int64_t n_g, int dtype);
 cudaError_t launch_plan(Ctrl* ctrl, RunConst rc, cudaStream_t s);
-cudaError_t launch_select(int mode, SelectArgs a, RunConst rc, cudaStream_t s);
+cudaError_t launch_stream(int mode, SelectArgs a, RunConst rc, cudaStream_t s);
+cudaError_t launch_finish(SelectArgs a, RunConst rc, cudaStream_t s);
 cudaError_t launch_union(UnionArgs a, RunConst rc, cudaStream_t s);
 cudaError_t launch_allreduce_local(const void* const* contribs, void* sum, const Ctrl* ctrl,
                                    const CountRec* counts, RunConst rc, cudaStream_t s);
@@ -111,12 +119,13 @@ size_t quantile_scratch_bytes();
 cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void* x0,
                                       const void* xw, int64_t n_g, int dtype, int32_t w,
                                       uint32_t* flag, cudaStream_t s);
+cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
 
-// selection modes of launch_select
+// modes of the stream kernel
 enum SelectMode {
-  kFused = 0,        // accumulate + select + compact (+ x update and finalize when n == 1)
+  kFused = 0,        // accumulate + select + stage (steady state)
   kAccumulate = 1,   // t = 0 without delta0: accumulate only
   kSelectOnly = 2,   // t = 0 without delta0: select over the partition only
 };

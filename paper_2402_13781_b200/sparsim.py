@@ -425,7 +425,8 @@ class Engine:
         s = A.exd_kernel_stats()
         check(self.L.exd_engine_kernel_stats(self.h, C.byref(s)))
         return {"select_launches": s.select_launches, "select_ms": s.select_ms, "steps": s.steps,
-                "kernel_launches": s.kernel_launches}
+                "kernel_launches": s.kernel_launches, "finish_launches": s.finish_launches,
+                "finish_ms": s.finish_ms}
 
     def reset_kernel_stats(self):
         check(self.L.exd_engine_reset_kernel_stats(self.h))
