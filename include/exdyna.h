@@ -254,6 +254,10 @@ int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host,
 int exd_engine_copy_in(exd_engine* h, int32_t w, int32_t which, const void* host,
                        int64_t n_elems);
 int exd_engine_kernel_stats(exd_engine* h, exd_kernel_stats* out);
+/* Turn per-kernel CUDA-event timing on/off (exd_options.profile_kernels).
+ * With it on, an event sits between the stream and finish kernels, which
+ * also serialises their otherwise overlapped (programmatic) launch. */
+int exd_engine_set_profile(exd_engine* h, int32_t on);
 int exd_engine_reset_kernel_stats(exd_engine* h);
 
 /* Writes a buffer larger than L2 on worker w's device (timing hygiene). */

@@ -9,7 +9,7 @@ import os
 from . import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libexdyna.so")
+LIB_PATH = os.environ.get("EXD_LIB") or os.path.join(HERE, "lib", "libexdyna.so")
 
 _lib = None
 
@@ -88,6 +88,7 @@ def lib():
     _sig(L, "exd_engine_copy_in", C.c_int, [P, C.c_int32, C.c_int32, P, C.c_int64])
     _sig(L, "exd_engine_kernel_stats", C.c_int, [P, C.POINTER(A.exd_kernel_stats)])
     _sig(L, "exd_engine_reset_kernel_stats", C.c_int, [P])
+    _sig(L, "exd_engine_set_profile", C.c_int, [P, C.c_int32])
     _sig(L, "exd_flush_l2", C.c_int, [C.c_int32, P])
     _lib = L
     return L
@@ -116,5 +117,6 @@ EXPORTED = [
     "exd_engine_local_workers", "exd_engine_first_rank", "exd_engine_iteration",
     "exd_engine_stream", "exd_engine_step", "exd_engine_step_async", "exd_engine_sync",
     "exd_engine_step_host", "exd_engine_get_state", "exd_engine_copy_out", "exd_engine_copy_in",
-    "exd_engine_kernel_stats", "exd_engine_reset_kernel_stats", "exd_flush_l2",
+    "exd_engine_kernel_stats", "exd_engine_reset_kernel_stats", "exd_engine_set_profile",
+    "exd_flush_l2",
 ]

@@ -36,14 +36,18 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile and link. `defines`/`out` build an experiment variant (e.g.
+    -DEXD_PROBE into lib/libexdyna_probe.so) without touching the product."""
+    lib_out = out or LIB
+    if not force and not defines and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
+    tag = "" if not defines else "_" + "_".join(d.lstrip("-D").lower() for d in defines)
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(LIBDIR, src.replace(".cu", tag + ".o"))
+        cmd = [NVCC] + FLAGS + list(defines) + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -53,14 +57,14 @@ def build(force=False, verbose=False):
         with open(obj + ".ptxas.txt", "w") as f:
             f.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

@@ -149,6 +149,21 @@ float round_up_float(double d) {
 
 size_t elem_size(int dtype) { return dtype == EXD_F64 ? 8 : 4; }
 
+// Granlund-Montgomery magic numbers for n / d with 31-bit n: with
+// l = ceil(log2 d), s = 31 + l and M = ceil(2^s / d) (<= 2^32),
+// floor(n * M / 2^s) == n / d for every n < 2^31, and n * M fits in 64 bits.
+void blk_magic(int64_t d, unsigned long long* magic, int32_t* shift) {
+  int l = 0;
+  while ((1LL << l) < d) ++l;
+  const int s = 31 + l;
+  const unsigned __int128 p = (unsigned __int128)1 << s;
+  *magic = (unsigned long long)((p + (unsigned __int128)(d - 1)) / (unsigned __int128)d);
+  *shift = s;
+}
+
+// per-step records stay on the device; the host copies the latest at sync
+constexpr int64_t kRecRing = 256;
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -171,8 +186,8 @@ struct Worker {
   int32_t* idx_global = nullptr;
   void* contrib = nullptr;
   void* grad_stage = nullptr;         // exd_engine_step_host staging
-  exd_record* rec_host = nullptr;     // mapped pinned
-  exd_record* rec_dev = nullptr;
+  exd_record* rec_host = nullptr;     // pinned: last record copied back at sync
+  exd_record* rec_dev = nullptr;      // device ring of kRecRing records (slot t % kRecRing)
   Plan plan0{};                       // host copy of the t = 0 plan
 };
 
@@ -300,6 +315,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     rc.min_blk = cfg.min_blk;
     rc.static_partitions = opt->static_partitions;
     rc.dtype = opt->dtype;
+    blk_magic(topo0.sz_blk, &rc.blk_magic, &rc.blk_shift);
     if (int r = alloc_zero(&wk.x, h->esz * ng)) return r;
     if (int r = alloc_zero(&wk.e, h->esz * ng)) return r;
     if (int r = alloc_zero((void**)&wk.idx, 4 * (size_t)h->cap_part)) return r;
@@ -322,9 +338,9 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     } else {
       wk.cnt = h->counts_all + wk.rank;
     }
-    CU(cudaHostAlloc((void**)&wk.rec_host, sizeof(exd_record), cudaHostAllocMapped));
+    CU(cudaHostAlloc((void**)&wk.rec_host, sizeof(exd_record), cudaHostAllocDefault));
     std::memset(wk.rec_host, 0, sizeof(exd_record));
-    CU(cudaHostGetDevicePointer((void**)&wk.rec_dev, wk.rec_host, 0));
+    if (int r = alloc_zero((void**)&wk.rec_dev, sizeof(exd_record) * kRecRing)) return r;
 
     // engine.cpp:68-87: x = 0, e = 0, topology, k_t = k/n, delta = delta0
     Ctrl c;
@@ -337,7 +353,8 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     c.topo = topo0;
     c.epoch = 1;
     wk.plan0 = host_plan(topo0, c.k_t, cfg, opt->static_partitions, wk.rank);
-    c.plan = wk.plan0;
+    c.plan[0] = wk.plan0;
+    c.plan[1] = wk.plan0;
     c.last = wk.plan0;
     CU(cudaMemcpy(wk.ctrl, &c, sizeof(c), cudaMemcpyHostToDevice));
     ctrls.push_back(wk.ctrl);
@@ -382,6 +399,7 @@ void teardown(exd_engine* h) {
     cudaFree(wk.grad_stage);
     if (h->dist) cudaFree(wk.cnt);
     cudaFreeHost(wk.rec_host);
+    cudaFree(wk.rec_dev);
   }
   cudaFree(h->counts_all);
   cudaFreeHost(h->counts_host);
@@ -445,9 +463,10 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.cta_norm = wk.cta_norm;
   a.ctrl = wk.ctrl;
   a.cnt_out = wk.cnt;
-  a.rec = wk.rec_dev;
+  a.rec = wk.rec_dev + (h->t % kRecRing);
   a.tile_base = 0;
   a.num_tiles = (int32_t)h->tiles;
+  a.t = h->t;
   return a;
 }
 
@@ -538,7 +557,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       f.x = wk.x;
       f.ctrl = wk.ctrl;
       f.counts = h->counts_all;
-      f.rec = wk.rec_dev;
+      f.rec = wk.rec_dev + (h->t % kRecRing);
       CU(launch_finalize(f, wk.rc, h->stream));
       h->stats.kernel_launches += 1;
     } else {
@@ -568,7 +587,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
         f.x = wk.x;
         f.ctrl = wk.ctrl;
         f.counts = h->counts_all;
-        f.rec = wk.rec_dev;
+        f.rec = wk.rec_dev + (h->t % kRecRing);
         CU(launch_finalize(f, wk.rc, h->stream));
         h->stats.kernel_launches += 1;
       h->stats.kernel_launches += 1;
@@ -615,6 +634,11 @@ int sync_engine(exd_engine* h, exd_record* out) {
                   (long long)h->verify_t, f >> 8, field);
     *h->verify_flag = 0;
     return set_err(EXD_EINVARIANT, msg);
+  }
+  if (h->has_record) {
+    for (auto& wk : h->w)
+      CU(cudaMemcpy(wk.rec_host, wk.rec_dev + ((h->t - 1) % kRecRing), sizeof(exd_record),
+                    cudaMemcpyDeviceToHost));
   }
   if (out) {
     if (!h->has_record) std::memset(out, 0, sizeof(*out));
@@ -843,8 +867,7 @@ int exd_engine_get_state(exd_engine* h, int32_t w, exd_worker_state* out) {
 int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host, int64_t cap,
                         int64_t* len) {
   if (w < 0 || w >= (int)h->w.size()) return set_err(EXD_EINVAL, "worker out of range");
-  CU(cudaSetDevice(h->device));
-  CU(cudaStreamSynchronize(h->stream));
+  if (int rc = sync_engine(h, nullptr)) return rc;
   Worker& wk = h->w[w];
   const exd_record& rec = *h->w[w].rec_host;
   int64_t n_el = 0;
@@ -900,6 +923,12 @@ int exd_engine_copy_in(exd_engine* h, int32_t w, int32_t which, const void* host
 int exd_engine_kernel_stats(exd_engine* h, exd_kernel_stats* out) {
   if (int rc = sync_engine(h, nullptr)) return rc;
   *out = h->stats;
+  return EXD_OK;
+}
+
+int exd_engine_set_profile(exd_engine* h, int32_t on) {
+  if (int rc = sync_engine(h, nullptr)) return rc;
+  h->opt.profile_kernels = on ? 1 : 0;
   return EXD_OK;
 }
 

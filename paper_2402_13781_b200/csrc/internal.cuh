@@ -30,7 +30,8 @@ struct Ctrl {
   int32_t has_delta;        // delta known (delta0 given or estimated)
   int64_t k_t[EXD_MAX_WORKERS];  // last gathered counts, rank order
   exd_topology topo;        // committed topology (reference's WorkerState::topology)
-  Plan plan;                // plan of step t
+  Plan plan[2];             // plan of step t lives in plan[t & 1]: the epilogue
+                            // writes step t+1's plan while step t's is still read
   Plan last;                // plan the last completed step ran with
   // fused-kernel bookkeeping (self-resetting)
   uint32_t ticket;          // dynamic tile ticket
@@ -55,6 +56,8 @@ struct RunConst {
   int64_t blk_move, min_blk;
   int32_t static_partitions;
   int32_t dtype;
+  unsigned long long blk_magic;  // j / sz_blk == (j * blk_magic) >> blk_shift for j < 2^31
+  int32_t blk_shift;
 };
 
 struct SelectArgs {
@@ -75,6 +78,7 @@ struct SelectArgs {
   exd_record* rec;          // fused n == 1: record (mapped host memory)
   int32_t tile_base;        // first tile covered by the stream launch
   int32_t num_tiles;        // tiles covered by the stream launch
+  int64_t t;                // the step these kernels run (selects plan[t & 1])
 };
 
 constexpr int kMaxCtas = 2048;
@@ -104,7 +108,6 @@ struct FinalizeArgs {
 // kernel launchers (kernels.cu)
 int tile_elems(int dtype);
 int64_t num_tiles(int64_t n_g, int dtype);
-cudaError_t launch_plan(Ctrl* ctrl, RunConst rc, cudaStream_t s);
 cudaError_t launch_stream(int mode, SelectArgs a, RunConst rc, cudaStream_t s);
 cudaError_t launch_finish(SelectArgs a, RunConst rc, cudaStream_t s);
 cudaError_t launch_union(UnionArgs a, RunConst rc, cudaStream_t s);

@@ -19,11 +19,26 @@
 // design levers are 128-bit coalesced loads, enough bytes in flight, one pass
 // over HBM, and grids sized to the 148 SMs.
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "internal.cuh"
 
 namespace exd {
+
+#ifdef EXD_PROBE
+// experiment build only: globaltimer stamps of the finish kernel's phases
+__device__ unsigned long long g_probe[64];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE(i) \
+  do { if (threadIdx.x == 0) g_probe[i] = gtimer(); } while (0)
+#else
+#define PROBE(i) do {} while (0)
+#endif
 
 namespace {
 
@@ -96,13 +111,15 @@ __device__ __forceinline__ float fabs_t(float v) { return fabsf(v); }
 __device__ __forceinline__ double fabs_t(double v) { return fabs(v); }
 
 // ---- control epilogue ----------------------------------------------------
-// Runs on ONE thread at the end of step t: the all-gather accounting
-// (collectives.cpp:29-45), the ledger row (engine.cpp:327-349), the threshold
-// rescale and k_t update (engine.cpp:206-213) and the plan of step t+1
-// (engine.cpp:125-131: rotate -> adjust -> allocate).
-// The epilogue works in place on the global control block with loops bounded
-// by n (no whole-struct copies), and is kept out of line so it does not
-// inflate the register allocation of the streaming kernels that call it.
+// The end of step t, once the gathered counts are known:
+//   record  the ledger row (collectives.cpp:29-45, engine.cpp:327-349)
+//   delta   threshold rescale, k_t update, topology commit (engine.cpp:206-213)
+//   plan    step t+1's rotate -> adjust -> allocate (engine.cpp:125-131)
+// It is sequential O(n) fp64/int64 work (IEEE divisions, 64-bit modulo) with
+// long dependency chains, so one CTA stages the control block in shared
+// memory (prefetched while the CTA's totals are still loading) and runs the
+// three independent parts on three different warps concurrently; step t+1's
+// plan goes to the other plan slot, so nothing else has to wait.
 __device__ __forceinline__ void copy_topo(exd_topology* dst, const exd_topology* src, int n) {
   dst->n = src->n;
   dst->sz_blk = src->sz_blk;
@@ -112,71 +129,136 @@ __device__ __forceinline__ void copy_topo(exd_topology* dst, const exd_topology*
   }
 }
 
-__device__ __noinline__ void make_plan(Ctrl* c, const RunConst& rc) {
-  Plan* p = &c->plan;
+// plan of step t_next from the topology committed by step t_next-1 and the
+// counts gathered at step t_next-1 (rank order)
+__device__ __noinline__ void make_plan(Plan* p, const exd_topology* base, const int64_t* k_rank,
+                                       int64_t t_next, const RunConst& rc) {
   const int n = rc.n;
-  copy_topo(&p->topo, &c->topo, n);
+  copy_topo(&p->topo, base, n);
   int32_t mv = 0, sk = 0;
   if (!rc.static_partitions) {
     int64_t kp[EXD_MAX_WORKERS];
-    rotate(c->k_t, c->t, n, kp);
+    rotate(k_rank, t_next, n, kp);
     adjust(p->topo, kp, rc.alpha, rc.blk_move, rc.min_blk, rc.n_g, &mv, &sk);
   }
   p->moves = mv;
   p->skips = sk;
   int64_t st, end;
-  p->partition = allocate(p->topo, c->t, rc.rank, rc.n_g, &st, &end);
+  p->partition = allocate(p->topo, t_next, rc.rank, rc.n_g, &st, &end);
   p->st = st;
   p->end = end;
 }
 
-__device__ __noinline__ void control_epilogue(Ctrl* c, const CountRec* counts, const RunConst& rc,
-                                              exd_record* rec) {
+__device__ __noinline__ void make_record(exd_record* rec, const int64_t* k_rank,
+                                         const double* norm2, int64_t t, double delta_used,
+                                         const Plan* cur, const RunConst& rc) {
   const int n = rc.n;
-  int64_t k_rank[EXD_MAX_WORKERS];
   double norm_sum = 0.0;
-  for (int r = 0; r < n; ++r) {
-    k_rank[r] = counts[r].k;
-    norm_sum = __dadd_rn(norm_sum, sqrt(counts[r].norm2));
-  }
+  for (int r = 0; r < n; ++r) norm_sum = __dadd_rn(norm_sum, sqrt(norm2[r]));
   exd_gather_stats gs;
   gather_stats(k_rank, n, &gs);
-  const double delta_used = c->delta;
-  if (rec) {
-    rec->t = c->t;
-    rec->k_prime = gs.k_prime;
-    rec->density = __ddiv_rn((double)gs.k_prime, (double)rc.n_g);
-    const int64_t diff = rc.k - gs.k_prime;
-    rec->eps = __ddiv_rn((double)(diff < 0 ? -diff : diff), (double)rc.n_g);
-    rec->m_t = gs.m_t;
-    rec->c_t = gs.c_t;
-    rec->f_t = gs.f_t;
-    rec->global_err = __ddiv_rn(norm_sum, (double)n);
-    rec->delta = delta_used;
-    rec->has_loss = 0;
-    rec->loss = 0.0;
-    rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
-    rec->union_count = gs.k_prime;
-    rec->n = n;
-    rec->adjust_moves = c->plan.moves;
-    rec->adjust_skips = c->plan.skips;
-    rec->cap_hits = 0;
-    rec->idle_workers = 0;
-    for (int r = 0; r < n; ++r) rec->k_rank[r] = k_rank[r];
+  rec->t = t;
+  rec->k_prime = gs.k_prime;
+  rec->density = __ddiv_rn((double)gs.k_prime, (double)rc.n_g);
+  const int64_t diff = rc.k - gs.k_prime;
+  rec->eps = __ddiv_rn((double)(diff < 0 ? -diff : diff), (double)rc.n_g);
+  rec->m_t = gs.m_t;
+  rec->c_t = gs.c_t;
+  rec->f_t = gs.f_t;
+  rec->global_err = __ddiv_rn(norm_sum, (double)n);
+  rec->delta = delta_used;
+  rec->has_loss = 0;
+  rec->reserved0 = 0;
+  rec->loss = 0.0;
+  rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
+  rec->union_count = gs.k_prime;
+  rec->n = n;
+  rec->adjust_moves = cur->moves;
+  rec->adjust_skips = cur->skips;
+  rec->cap_hits = 0;
+  rec->idle_workers = 0;
+  rec->reserved1 = 0;
+  for (int r = 0; r < n; ++r) rec->k_rank[r] = k_rank[r];
+}
+
+__device__ __noinline__ void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc) {
+  const int n = rc.n;
+  int64_t kp = 0;
+  for (int r = 0; r < n; ++r) {
+    kp += k_rank[r];
+    c->k_t[r] = k_rank[r];
   }
-  // apply_phase control (engine.cpp:211-213)
-  c->delta = scale_threshold(rc.k, gs.k_prime, c->delta, rc.beta, rc.gamma);
+  c->delta = scale_threshold(rc.k, kp, c->delta, rc.beta, rc.gamma);
   c->thr_f = thr_of(c->delta);
-  for (int r = 0; r < n; ++r) c->k_t[r] = k_rank[r];
-  copy_topo(&c->topo, &c->plan.topo, n);
-  copy_topo(&c->last.topo, &c->plan.topo, n);
-  c->last.st = c->plan.st;
-  c->last.end = c->plan.end;
-  c->last.partition = c->plan.partition;
-  c->last.moves = c->plan.moves;
-  c->last.skips = c->plan.skips;
+  const Plan* cur = &c->plan[c->t & 1];
+  copy_topo(&c->topo, &cur->topo, n);
+  copy_topo(&c->last.topo, &cur->topo, n);
+  c->last.st = cur->st;
+  c->last.end = cur->end;
+  c->last.partition = cur->partition;
+  c->last.moves = cur->moves;
+  c->last.skips = cur->skips;
   c->t += 1;
-  make_plan(c, rc);
+}
+
+// Shared-memory staging of the control block for one CTA.
+struct EpiShared {
+  Ctrl c;
+  exd_record rec;
+  int64_t k_rank[EXD_MAX_WORKERS];
+  double norm2[EXD_MAX_WORKERS];
+};
+
+__device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
+  static_assert(sizeof(Ctrl) % 8 == 0 && sizeof(exd_record) % 8 == 0, "word copies");
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
+  const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(cg);
+  constexpr int W = (int)(sizeof(Ctrl) / 8);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < W; i += blockDim.x) sw[i] = __ldcg(&gw[i]);
+}
+
+// Run the epilogue on the staged copy (sh.c, sh.k_rank, sh.norm2 filled;
+// caller synced), then write the control block and the record back. Whole CTA.
+__device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const RunConst& rc,
+                                              exd_record* rec_out) {
+  const int tid = threadIdx.x;
+  const int64_t t = sh.c.t;
+  const double delta_used = sh.c.delta;
+  __syncthreads();  // everyone read t / delta before warp 0 changes them
+  if (tid == 0) {
+    advance_delta(&sh.c, sh.k_rank, rc);
+    sh.c.done = 0;
+  } else if (tid == 32) {
+    make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, t + 1, rc);
+  } else if (tid == 64 && rec_out) {
+    make_record(&sh.rec, sh.k_rank, sh.norm2, t, delta_used, &sh.c.plan[t & 1], rc);
+  }
+  __syncthreads();
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
+  unsigned long long* gw = reinterpret_cast<unsigned long long*>(cg);
+  for (int i = tid; i < (int)(sizeof(Ctrl) / 8); i += blockDim.x) gw[i] = sw[i];
+  if (rec_out) {
+    const unsigned long long* rs = reinterpret_cast<const unsigned long long*>(&sh.rec);
+    unsigned long long* rd = reinterpret_cast<unsigned long long*>(rec_out);
+    const int words = (int)((offsetof(exd_record, k_rank) + 8 * rc.n + 7) / 8);
+    for (int i = tid; i < words; i += blockDim.x) rd[i] = rs[i];
+  }
+}
+
+// Standalone form: load, run, store (finalize kernel, block 0).
+__device__ __forceinline__ void control_epilogue_cta(Ctrl* cg, const CountRec* counts,
+                                                     const RunConst& rc, exd_record* rec_out) {
+  __shared__ EpiShared sh;
+  epi_load(sh, cg);
+  for (int r = threadIdx.x; r < rc.n; r += blockDim.x) {
+    sh.k_rank[r] = __ldcg(&counts[r].k);
+    sh.norm2[r] = __ldcg(&counts[r].norm2);
+  }
+  __syncthreads();
+  PROBE(4);
+  epi_run_store(sh, cg, rc, rec_out);
+  PROBE(5);
 }
 
 // ---- K1: the streaming kernel (accumulate / select / stage) -----------------
@@ -192,6 +274,21 @@ __device__ __noinline__ void control_epilogue(Ctrl* c, const CountRec* counts, c
 // a pure stream: it runs at the measured copy bandwidth.
 template <typename T> __host__ __device__ constexpr int chunk_of() { return 32 * Vec<T>::N * kUnroll; }
 
+template <typename V>
+__device__ __forceinline__ V warp_sum(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ExDyna block of element j: min(j / sz_blk, n_b - 1) (the last block absorbs
+// the tail, partition.cpp:60-68), by multiply-shift with the run's magic
+// numbers (exact for j < 2^31; see blk_magic in engine.cu)
+__device__ __forceinline__ uint32_t block_of(uint32_t j, const RunConst& rc) {
+  const uint32_t b = (uint32_t)(((unsigned long long)j * rc.blk_magic) >> rc.blk_shift);
+  return b < (uint32_t)(rc.n_b - 1) ? b : (uint32_t)(rc.n_b - 1);
+}
+
 template <typename T, int MODE, bool UNIT>
 __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunConst rc) {
   constexpr int VN = Vec<T>::N;
@@ -205,32 +302,41 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
   const Ctrl* ctrl = a.ctrl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = a.tile_base + (int)blockIdx.x;
-  const int chunk = tile * kWarps + warp;
-  const int64_t n_g = rc.n_g;
-  const int64_t cbeg = (int64_t)chunk * CH;
+  if (blockIdx.x == 0) PROBE(16);
+  if (blockIdx.x == gridDim.x - 1) PROBE(17);
+  // programmatic dependent launch: once every CTA of this grid has started,
+  // the finish kernel may be scheduled (it waits for our completion before
+  // reading anything we write)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // n_g < 2^31 (checked at engine creation): 32-bit element indices throughout
+  const uint32_t n_g = (uint32_t)rc.n_g;
+  const uint32_t cbeg = (uint32_t)(tile * kWarps + warp) * CH;
+  const uint32_t lbeg = cbeg + lane * VN;  // this lane's first element
   T* e = static_cast<T*>(a.e);
   const T* g = static_cast<const T*>(a.g);
 
   // issue every load of the chunk before any use: 2 * kUnroll 16 B loads in
   // flight per lane
   T ev[kUnroll][VN], gv[kUnroll][VN];
-  if (cbeg + CH <= n_g) {
+  const bool full = cbeg + CH <= n_g;
+  if (full) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      vload<T>(e + cbeg + u * 32 * VN + lane * VN, ev[u]);
-      if (ACCUM) vload<T>(g + cbeg + u * 32 * VN + lane * VN, gv[u]);
+      vload<T>(e + lbeg + u * 32 * VN, ev[u]);
+      if (ACCUM) vload<T>(g + lbeg + u * 32 * VN, gv[u]);
     }
   } else {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
       for (int c = 0; c < VN; ++c) {
-        const int64_t j = cbeg + u * 32 * VN + lane * VN + c;
+        const uint32_t j = lbeg + u * 32 * VN + c;
         ev[u][c] = j < n_g ? e[j] : T(0);
         gv[u][c] = (ACCUM && j < n_g) ? g[j] : T(0);
       }
   }
-  const int64_t st = ctrl->plan.st, end = ctrl->plan.end;
+  const Plan& plan = ctrl->plan[a.t & 1];
+  const uint32_t st = (uint32_t)plan.st, end = (uint32_t)plan.end;
 
   T v[kUnroll][VN];
   double nrm = 0.0;
@@ -263,34 +369,32 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
         for (int c = 0; c < VN; ++c)
           flags |= (uint32_t)(fabs_t(v[u][c]) >= thr) << (u * VN + c);
     } else {
-      const int lo = (int)(st > cbeg ? st - cbeg : 0);
-      const int hi = (int)(end - cbeg < CH ? end - cbeg : CH);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
-          const int off = u * 32 * VN + lane * VN + c;
-          flags |= (uint32_t)(off >= lo && off < hi && fabs_t(v[u][c]) >= thr) << (u * VN + c);
+          const uint32_t j = lbeg + u * 32 * VN + c;
+          flags |= (uint32_t)(j >= st && j < end && fabs_t(v[u][c]) >= thr) << (u * VN + c);
         }
     }
   }
 
   // residual write-back: acc, or 0 where selected (own partition cleared here)
   if (ACCUM) {
-    if (cbeg + CH <= n_g) {
+    if (full) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         T w[VN];
 #pragma unroll
         for (int c = 0; c < VN; ++c) w[c] = (flags >> (u * VN + c)) & 1u ? T(0) : v[u][c];
-        vstore<T>(e + cbeg + u * 32 * VN + lane * VN, w);
+        vstore<T>(e + lbeg + u * 32 * VN, w);
       }
     } else {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
-          const int64_t j = cbeg + u * 32 * VN + lane * VN + c;
+          const uint32_t j = lbeg + u * 32 * VN + c;
           if (j < n_g) e[j] = (flags >> (u * VN + c)) & 1u ? T(0) : v[u][c];
         }
     }
@@ -299,20 +403,17 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
     for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
       for (int c = 0; c < VN; ++c)
-        if ((flags >> (u * VN + c)) & 1u) e[cbeg + u * 32 * VN + lane * VN + c] = T(0);
+        if ((flags >> (u * VN + c)) & 1u) e[lbeg + u * 32 * VN + c] = T(0);
   }
 
   // warp-level ordered compaction of the chunk into its staging run
   int running = 0;
   if (sel_chunk) {
     const uint32_t lt = (1u << lane) - 1u;
-    const int64_t sbase = (cbeg - (st / CH) * CH);  // chunk's run in the staging buffer
-    const int64_t sz_blk = ctrl->plan.topo.sz_blk;
-    const int64_t lo = cbeg > st ? cbeg : st;
-    const int64_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
-    int64_t b_lo = lo / sz_blk, b_hi = hi / sz_blk;
-    b_lo = b_lo > rc.n_b - 1 ? rc.n_b - 1 : b_lo;
-    b_hi = b_hi > rc.n_b - 1 ? rc.n_b - 1 : b_hi;
+    const uint32_t sbase = cbeg - (st / CH) * CH;  // chunk's run in the staging buffer
+    const uint32_t lo = cbeg > st ? cbeg : st;
+    const uint32_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
+    const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
     const bool split = b_lo != b_hi;
     T* sv = static_cast<T*>(a.stage_val);
 #pragma unroll
@@ -323,17 +424,17 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
       const uint32_t b1 = __ballot_sync(0xffffffffu, cnt & 2u);
       const uint32_t b2 = __ballot_sync(0xffffffffu, cnt & 4u);
       if (nib) {
-        int pos = running + (int)(__popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt));
+        uint32_t pos = sbase + running + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
-            const int64_t j = cbeg + u * 32 * VN + lane * VN + c;
-            a.stage_idx[sbase + pos] = (int32_t)j;
-            sv[sbase + pos] = v[u][c];
-            if (split) {
-              int64_t b = j / sz_blk;
-              atomicAdd(&a.blk_counts[b > rc.n_b - 1 ? rc.n_b - 1 : b], 1);
-            }
+            const uint32_t j = lbeg + u * 32 * VN + c;
+            a.stage_idx[pos] = (int32_t)j;
+            sv[pos] = v[u][c];
+            // n == 1: the finish kernel will read-modify-write x[j]; pull the
+            // line into L2 now, off everyone's critical path
+            if (rc.n == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<T*>(a.x) + j));
+            if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
             ++pos;
           }
         }
@@ -342,12 +443,9 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
     }
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
   }
-  if (SELECT && lane == 0) a.chunk_count[chunk] = running;
+  if (SELECT && lane == 0) a.chunk_count[tile * kWarps + warp] = running;
 
-  if (ACCUM) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-  }
+  if (ACCUM) nrm = warp_sum(nrm);
   if (lane == 0) {
     s_norm[warp] = nrm;
     s_cnt[warp] = running;
@@ -372,27 +470,28 @@ __global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunCo
 // ---- K2: the finish kernel ----------------------------------------------------
 // Turns per-tile / per-chunk counts into global offsets and moves the staged
 // runs to the ascending (index, value) lists; applies x -= g/n (engine.cpp:215)
-// when n == 1 (the all-reduce is the identity); reduces the per-tile norm
-// partials in a fixed order; the last CTA publishes {k_i, ||e||^2} and, for
-// n == 1, runs the control epilogue. Every reduction here is written as wide,
-// independent loads: the kernel moves little data and is latency-bound.
-template <typename V>
-__device__ __forceinline__ V warp_sum(V v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+// when n == 1 (the all-reduce is the identity). One extra CTA (the last block)
+// reduces the per-tile counts and norm partials in a fixed order, publishes
+// {k_i, ||e||^2} and, for n == 1, runs the control epilogue; it never waits for
+// the copy CTAs because step t+1's plan goes to the other plan slot.
+// Everything is latency-bound here, so every phase issues its loads wide and
+// independent before using them.
+constexpr int kSumUnroll = 12;
 
-// sum of cnt[lo, hi) (int32) by the whole CTA, 4 independent loads per thread per round
-__device__ __forceinline__ int64_t cta_sum_counts(const int32_t* cnt, int lo, int hi, int64_t* red) {
+// sum of cnt[lo, hi) (int32) by the whole CTA: kSumUnroll independent loads per
+// thread per round (one round covers 3072 tiles)
+__device__ __forceinline__ int64_t cta_sum_counts(const int32_t* __restrict__ cnt, int lo, int hi,
+                                                  int64_t* red) {
   int64_t s = 0;
-  for (int i = lo + (int)threadIdx.x; i < hi; i += 4 * kThreads) {
-    const int i1 = i + kThreads, i2 = i + 2 * kThreads, i3 = i + 3 * kThreads;
-    const int v0 = __ldcg(&cnt[i]);
-    const int v1 = i1 < hi ? __ldcg(&cnt[i1]) : 0;
-    const int v2 = i2 < hi ? __ldcg(&cnt[i2]) : 0;
-    const int v3 = i3 < hi ? __ldcg(&cnt[i3]) : 0;
-    s += (int64_t)v0 + v1 + v2 + v3;
+  for (int i = lo + (int)threadIdx.x; i < hi; i += kSumUnroll * kThreads) {
+    int v[kSumUnroll];
+#pragma unroll
+    for (int k = 0; k < kSumUnroll; ++k) {
+      const int ik = i + k * kThreads;
+      v[k] = ik < hi ? __ldcg(&cnt[ik]) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kSumUnroll; ++k) s += v[k];
   }
   s = warp_sum(s);
   __syncthreads();
@@ -404,6 +503,8 @@ __device__ __forceinline__ int64_t cta_sum_counts(const int32_t* cnt, int lo, in
   return t;
 }
 
+constexpr int kCopyUnroll = 4;
+
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst rc) {
   constexpr int CH = chunk_of<T>();
@@ -412,36 +513,103 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   __shared__ double s_dred[kWarps];
   __shared__ int s_off[kThreads + 1];
   __shared__ int s_wtot[kWarps];
-  __shared__ bool s_last;
 
   Ctrl* ctrl = a.ctrl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, r = blockIdx.x;
+  // block 0 is the epilogue CTA (dispatched first, so its control-block
+  // prefetch overlaps the stream kernel's tail); blocks 1..G copy
+  const int G = gridDim.x - 1, r = (int)blockIdx.x - 1;
   const int64_t n_g = rc.n_g;
-  const int64_t st = ctrl->plan.st, end = ctrl->plan.end;
+  const Plan& plan = ctrl->plan[a.t & 1];
+  const int64_t st = plan.st, end = plan.end;
   const int ft = (int)(st / TILE), lt = (int)((end - 1) / TILE);
+
+  if (r < 0) {
+    PROBE(0);
+    // ---- epilogue CTA: prefetch the control block (n == 1), then the totals
+    // in a fixed order, then the control epilogue
+    __shared__ EpiShared esh;
+    if (FUSED) epi_load(esh, ctrl);  // the stream kernel never writes the control block
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // one round of wide independent loads for both totals
+    const int nt = (int)((n_g + TILE - 1) / TILE);
+    double pn = 0.0;
+    int64_t pk = 0;
+    for (int i = tid; i < nt; i += kSumUnroll * kThreads) {
+      double v[kSumUnroll];
+      int c[kSumUnroll];
+#pragma unroll
+      for (int k = 0; k < kSumUnroll; ++k) {
+        const int ik = i + k * kThreads;
+        v[k] = ik < nt ? __ldcg(&a.tile_norm[ik]) : 0.0;
+        c[k] = (ik < nt && ik >= ft && ik <= lt) ? __ldcg(&a.tile_count[ik]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < kSumUnroll; ++k) {
+        pn += v[k];
+        pk += c[k];
+      }
+    }
+    PROBE(1);
+    pn = warp_sum(pn);
+    pk = warp_sum(pk);
+    if (lane == 0) {
+      s_dred[warp] = pn;
+      s_red[warp] = pk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double n2 = 0.0;
+      int64_t kt = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        n2 += s_dred[w];
+        kt += s_red[w];
+      }
+      a.cnt_out->k = kt;
+      a.cnt_out->norm2 = n2;
+      if (FUSED) {
+        esh.c.k_local = kt;
+        esh.c.norm2 = n2;
+        esh.k_rank[0] = kt;
+        esh.norm2[0] = n2;
+      } else {
+        ctrl->k_local = kt;
+        ctrl->norm2 = n2;
+      }
+    }
+    if (FUSED) {
+      __syncthreads();
+      PROBE(2);
+      epi_run_store(esh, ctrl, rc, a.rec);
+    }
+    PROBE(3);
+    return;
+  }
+
+  // ---- copy CTAs: a static contiguous range of the partition's tiles
+  if (r == 0) PROBE(8);
   const int ntp = lt - ft + 1;
   const int t0 = ft + (int)(((int64_t)ntp * r) / G);
   const int t1 = ft + (int)(((int64_t)ntp * (r + 1)) / G);
   const int64_t fc = st / CH;
-
-  // fixed-order norm partial over a static range of ALL tiles (issued first:
-  // independent of everything below)
-  const int nt = (int)((n_g + TILE - 1) / TILE);
-  const int n0 = (int)(((int64_t)nt * r) / G), n1 = (int)(((int64_t)nt * (r + 1)) / G);
-  double sn = 0.0;
-  for (int i = n0 + tid; i < n1; i += kThreads) sn += __ldcg(&a.tile_norm[i]);
-
-  // global offset of this CTA's first tile
+  const int nch = (t1 - t0) * kWarps;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's counts and runs
+  // chunk counts of the first batch, issued before the prefix sum (independent)
+  int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
   const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
+  if (r == 0) PROBE(9);
+  if (r == G - 1) PROBE(10);
 
-  T* val = static_cast<T*>(a.val);
-  T* x = static_cast<T*>(a.x);
-  const T* sv = static_cast<const T*>(a.stage_val);
+  T* __restrict__ val = static_cast<T*>(a.val);
+  T* __restrict__ x = static_cast<T*>(a.x);
+  int32_t* __restrict__ idx = a.idx;
+  const int32_t* __restrict__ sidx = a.stage_idx;
+  const T* __restrict__ sv = static_cast<const T*>(a.stage_val);
   int64_t running = base;
-  for (int cb = t0 * kWarps; cb < t1 * kWarps; cb += kThreads) {
-    const int nb = (t1 * kWarps - cb) < kThreads ? (t1 * kWarps - cb) : kThreads;
-    const int cnt = tid < nb ? __ldcg(&a.chunk_count[cb + tid]) : 0;
+  for (int cb = 0; cb < nch; cb += kThreads) {
+    const int nb = nch - cb < kThreads ? nch - cb : kThreads;
+    if (cb) cnt = tid < nb ? __ldcg(&a.chunk_count[t0 * kWarps + cb + tid]) : 0;
     // block exclusive scan of the chunk counts
     int incl = cnt;
 #pragma unroll
@@ -458,62 +626,48 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
       btot += s_wtot[w];
     }
     s_off[tid] = wpre + incl - cnt;
-    if (tid == 0) s_off[kThreads] = btot;
     __syncthreads();
-    // flattened copy: entry i of the batch lives in chunk k with
-    // s_off[k] <= i < s_off[k+1] (empty chunks have equal bounds)
-    for (int i = tid; i < btot; i += kThreads) {
-      int lo = 0, hi = nb;  // find the last k with s_off[k] <= i
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_off[mid] <= i) lo = mid; else hi = mid;
+    // flattened copy, kCopyUnroll entries per thread in flight: entry i of the
+    // batch lives in chunk k with s_off[k] <= i < s_off[k + 1]
+    const int64_t cbase = (int64_t)(t0 * kWarps + cb) - fc;
+    for (int i0 = tid; i0 < btot; i0 += kCopyUnroll * kThreads) {
+      int32_t jj[kCopyUnroll];
+      T vv[kCopyUnroll];
+      T xx[kCopyUnroll];
+#pragma unroll
+      for (int q = 0; q < kCopyUnroll; ++q) {
+        const int i = i0 + q * kThreads;
+        if (i < btot) {
+          int lo = 0, hi = nb;  // last k with s_off[k] <= i
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= i) lo = mid; else hi = mid;
+          }
+          const int64_t src = (cbase + lo) * CH + (i - s_off[lo]);
+          jj[q] = __ldcg(&sidx[src]);
+          vv[q] = __ldcg(&sv[src]);
+        }
       }
-      const int64_t src = (int64_t)(cb + lo - fc) * CH + (i - s_off[lo]);
-      const int32_t j = __ldcg(&a.stage_idx[src]);
-      const T vv = __ldcg(&sv[src]);
-      a.idx[running + i] = j;
-      val[running + i] = vv;
-      if (FUSED) x[j] = apply_update<T>(x[j], vv, rc.n);
+      if (FUSED) {
+#pragma unroll
+        for (int q = 0; q < kCopyUnroll; ++q)
+          if (i0 + q * kThreads < btot) xx[q] = x[jj[q]];
+      }
+#pragma unroll
+      for (int q = 0; q < kCopyUnroll; ++q) {
+        const int i = i0 + q * kThreads;
+        if (i < btot) {
+          idx[running + i] = jj[q];
+          val[running + i] = vv[q];
+          if (FUSED) x[jj[q]] = apply_update<T>(xx[q], vv[q], rc.n);
+        }
+      }
     }
     running += btot;
     __syncthreads();
   }
-
-  sn = warp_sum(sn);
-  if (lane == 0) s_dred[warp] = sn;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += s_dred[w];
-    a.cta_norm[r] = t;
-    __threadfence();
-    s_last = atomicAdd(&ctrl->done, 1u) == (unsigned)G - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int64_t kt = cta_sum_counts(a.tile_count, ft, lt + 1, s_red);
-  // fixed-order final norm: thread q sums cta_norm[q], [q+256], ... then a
-  // fixed warp tree
-  double pn = 0.0;
-  for (int q = tid; q < G; q += kThreads) pn += __ldcg(&a.cta_norm[q]);
-  pn = warp_sum(pn);
-  __syncthreads();
-  if (lane == 0) s_dred[warp] = pn;
-  __syncthreads();
-  if (tid == 0) {
-    double n2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) n2 += s_dred[w];
-    ctrl->k_local = kt;
-    ctrl->norm2 = n2;
-    a.cnt_out->k = kt;
-    a.cnt_out->norm2 = n2;
-    if (FUSED) control_epilogue(ctrl, a.cnt_out, rc, a.rec);
-    ctrl->done = 0;
-    __threadfence();
-  }
+  if (r == 0) PROBE(11);
+  if (r == G - 1) PROBE(12);
 }
 
 template <typename T, bool UNIT>
@@ -542,18 +696,25 @@ cudaError_t launch_finish_t(const SelectArgs& a, const RunConst& rc, cudaStream_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cap = sms * 2 > kMaxCtas ? kMaxCtas : sms * 2;
   }
-  // the partition's tile count is device-resident; size for the whole vector
+  // the partition's tile count is device-resident; size for the whole vector,
+  // plus one epilogue CTA
   const int64_t nt = num_tiles(rc.n_g, rc.dtype);
   int grid = nt < cap ? (int)nt : cap;
   if (grid < 1) grid = 1;
-  if (rc.n == 1) finish_kernel<T, true><<<grid, kThreads, 0, s>>>(a, rc);
-  else finish_kernel<T, false><<<grid, kThreads, 0, s>>>(a, rc);
-  return cudaGetLastError();
-}
-
-// ---- initial plan (t = 0) ---------------------------------------------------
-__global__ void plan_kernel(Ctrl* c, RunConst rc) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) make_plan(c, rc);
+  // programmatic stream serialization: overlaps this launch with the tail of
+  // the stream kernel (see griddepcontrol in both kernels)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid + 1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (rc.n == 1) return cudaLaunchKernelEx(&cfg, finish_kernel<T, true>, a, rc);
+  return cudaLaunchKernelEx(&cfg, finish_kernel<T, false>, a, rc);
 }
 
 // ---- K4+K5: union + contributions + clear -----------------------------------
@@ -630,7 +791,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a, RunConst 
     const int32_t j = a.idx_global[pos];
     x[j] = apply_update<T>(x[j], g[pos], rc.n);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) control_epilogue(a.ctrl, a.counts, rc, a.rec);
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    control_epilogue_cta(a.ctrl, a.counts, rc, a.rec);
+  }
 }
 
 // ---- delta0 broadcast into every worker's control block ---------------------
@@ -828,6 +992,12 @@ static __global__ void l2_read_kernel(const float4* __restrict__ p, int64_t n4, 
   if (s == 1234.5f) atomicAdd(sink, 1);
 }
 
+#ifdef EXD_PROBE
+extern "C" int exd_debug_probe(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_probe, sizeof(g_probe));
+}
+#endif
+
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s) {
   cudaError_t err = cudaMemsetAsync(buf, 1, bytes, s);
   if (err != cudaSuccess) return err;
@@ -842,11 +1012,6 @@ int tile_elems(int dtype) { return dtype == EXD_F64 ? tile_of<double>() : tile_o
 int64_t num_tiles(int64_t n_g, int dtype) {
   const int t = tile_elems(dtype);
   return (n_g + t - 1) / t;
-}
-
-cudaError_t launch_plan(Ctrl* ctrl, RunConst rc, cudaStream_t s) {
-  plan_kernel<<<1, 32, 0, s>>>(ctrl, rc);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_stream(int mode, SelectArgs a, RunConst rc, cudaStream_t s) {

@@ -431,6 +431,9 @@ class Engine:
     def reset_kernel_stats(self):
         check(self.L.exd_engine_reset_kernel_stats(self.h))
 
+    def set_profile(self, on: bool):
+        check(self.L.exd_engine_set_profile(self.h, int(on)))
+
 
 # ------------------------------------------------------------- workloads ----
 @dataclass

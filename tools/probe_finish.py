@@ -1,0 +1,37 @@
+"""Experiment: phase timestamps (globaltimer) of the stream/finish kernels.
+Build: python -c "from paper_2402_13781_b200 import build as B; B.build(defines=['-DEXD_PROBE'], out=B.LIBDIR+'/libexdyna_probe.so')"
+Run:   EXD_LIB=paper_2402_13781_b200/lib/libexdyna_probe.so python tools/probe_finish.py [--n 1]
+"""
+import argparse, ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ap = argparse.ArgumentParser(); ap.add_argument("--n", type=int, default=1); a = ap.parse_args()
+import torch
+from paper_2402_13781_b200 import sparsim as S
+from paper_2402_13781_b200._lib import lib
+L = lib()
+L.exd_debug_probe.argtypes = [C.POINTER(C.c_uint64)]
+n_g = 11_200_000
+eng = S.Engine(S.SparsifierConfig(n=a.n, n_g=n_g, n_b=256, d=0.01, seed=7),
+               S.EngineOptions(verify_replication=False))
+src = S.SyntheticStream(S.StreamSpec(n_g=n_g, seed=7))
+pool = [[torch.empty(n_g, device="cuda") for _ in range(a.n)] for _ in range(2)]
+for i, bs in enumerate(pool):
+    for r, b in enumerate(bs):
+        src.gradient(i, r, b, "f32", eng.stream())
+torch.cuda.synchronize()
+for i in range(300):
+    eng.step_async(pool[i % 2])
+eng.sync()
+names = {0: "epi_start", 1: "epi_sums", 2: "epi_pre_cta", 4: "epi_ctrl_loaded", 5: "epi_computed",
+         3: "epi_end", 8: "copy0_start", 9: "copy0_base", 10: "copyL_base", 11: "copy0_end",
+         12: "copyL_end", 16: "k1_first_cta", 17: "k1_last_cta"}
+rows = []
+for i in range(5):
+    S.flush_l2(0, eng.stream())
+    eng.step(pool[i % 2])
+    buf = (C.c_uint64 * 64)()
+    L.exd_debug_probe(buf)
+    t0 = buf[16]
+    rows.append({names[k]: (buf[k] - t0) / 1e3 for k in names if buf[k]})
+for r in rows:
+    print("  ".join(f"{k}={v:.1f}" for k, v in sorted(r.items(), key=lambda kv: kv[1])))

@@ -42,12 +42,26 @@ def main():
         eng.step_async(pool[i % 2])
     rec = eng.sync()
     st = eng.kernel_stats()
+    # whole-step time with profiling off (stream->finish launches overlap)
+    eng.set_profile(False)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    xs = torch.cuda.ExternalStream(eng.stream())
+    for i in range(a.steps):
+        if a.flush:
+            S.flush_l2(0, eng.stream())
+        evs[i][0].record(xs)
+        eng.step_async(pool[i % 2])
+        evs[i][1].record(xs)
+    eng.sync()
+    step_us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in evs)
     ms = st["select_ms"] / max(1, st["select_launches"])
     byt = (12 if a.dtype == "f32" else 24) * a.n_g
     fin = st["finish_ms"] / max(1, st["finish_launches"])
     print(f"n={a.n} n_g={a.n_g} {a.dtype} stream avg {ms*1e3:.1f} us over {st['select_launches']} launches "
           f"-> {byt/ms/1e6:.0f} GB/s ({byt/a.n_g:.0f} B/elem); finish avg {fin*1e3:.1f} us; "
-          f"k'={rec.k_prime} f_t={rec.f_t:.3f} t={rec.t}")
+          f"k'={rec.k_prime} f_t={rec.f_t:.3f} t={rec.t}; step median {step_us[len(step_us)//2]:.1f} us "
+          f"(min {step_us[0]:.1f})")
 
 
 if __name__ == "__main__":
