@@ -121,6 +121,17 @@ def ncu_traffic():
         return None
 
 
+def max_over_ranks(values, dist=None):
+    """Max of each timing over all ranks (the contract's whole-job time): the
+    slowest rank defines the step. `dist` is torch.distributed or None."""
+    if dist is None:
+        return [float(v) for v in values]
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
 # ------------------------------------------------------- reference (CPU) ----
 def reference_ms_per_step(n, steps, warmup, pool=None):
     """Time the unmodified reference's Engine::step() (oracle/_ref) on this host."""
@@ -214,16 +225,30 @@ def run_ours(args):
 
     clocks = ClockSampler(local)
     clocks.start()
-    # warm-up: at least W steps and ~1.5 s so the clock samples see load
-    t_end = time.time() + 1.5
+    # warm-up: W steps, then enough more for ~1.5 s under load so the clock
+    # samples see it; every rank must run the same number of steps (each step
+    # is a set of collectives), so rank 0 decides and broadcasts the count
     i = 0
-    while i < args.warmup or time.time() < t_end:
-        src.gradient(i, rank, bufs[i % POOL], "f32", eng.stream())  # fresh g_t (untimed)
-        eng.step_async([bufs[i % POOL]])
-        if i % 16 == 15:
-            eng.sync()
-        i += 1
-    eng.sync()
+
+    def run_steps(k):
+        nonlocal i
+        for _ in range(k):
+            src.gradient(i, rank, bufs[i % POOL], "f32", eng.stream())  # fresh g_t (untimed)
+            eng.step_async([bufs[i % POOL]])
+            if i % 16 == 15:
+                eng.sync()
+            i += 1
+        eng.sync()
+
+    t0 = time.time()
+    run_steps(args.warmup)
+    per_step = max((time.time() - t0) / args.warmup, 1e-5)
+    extra = [int(min(1.5 / per_step, 200_000))]
+    if dist:
+        t = torch.tensor(extra)
+        dist.broadcast(t, src=0)
+        extra = [int(t[0])]
+    run_steps(extra[0])
     eng.reset_kernel_stats()
     launches0 = eng.kernel_stats()["kernel_launches"]
     barrier()
@@ -266,10 +291,7 @@ def run_ours(args):
     sel_ms = ks2["select_ms"] / max(ks2["select_launches"], 1)
     fin_ms = ks2["finish_ms"] / max(ks2["finish_launches"], 1)
     eng.set_profile(False)
-    if dist:
-        t = torch.tensor([total_ms, sel_ms, fin_ms])
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, sel_ms, fin_ms = float(t[0]), float(t[1]), float(t[2])
+    total_ms, sel_ms, fin_ms = max_over_ranks([total_ms, sel_ms, fin_ms], dist)
     ms = total_ms / args.steps
 
     # ---- e2e: public API from pinned host buffers, H2D inside the region ----
@@ -294,11 +316,7 @@ def run_ours(args):
         check(L.exd_engine_step_host(eng.h, ptrs, C.byref(rec)))  # returns with the record on the host
         ev2[k][1].record(stream)
     barrier()
-    e2e_total = sum(a.elapsed_time(b) for a, b in ev2)
-    if dist:
-        t = torch.tensor([e2e_total])
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t[0])
+    e2e_total = max_over_ranks([sum(a.elapsed_time(b) for a, b in ev2)], dist)[0]
     e2e_ms = e2e_total / e2e_steps
     clk = clocks.stop()
 

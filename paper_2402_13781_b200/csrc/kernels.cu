@@ -44,8 +44,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;
-static_assert(kUnroll * kWarps == 32, "the block scan assumes one warp of partials");
+#ifndef EXD_K1_UNROLL
+#define EXD_K1_UNROLL 4
+#endif
+#ifndef EXD_K1_MINB
+#define EXD_K1_MINB 4
+#endif
+constexpr int kUnroll = EXD_K1_UNROLL;  // 16 B vectors per lane per stream in the stream kernel
+
 
 template <typename T> struct Vec;
 template <> struct Vec<float> {
@@ -290,7 +296,7 @@ __device__ __forceinline__ uint32_t block_of(uint32_t j, const RunConst& rc) {
 }
 
 template <typename T, int MODE, bool UNIT>
-__global__ void __launch_bounds__(kThreads, 4) stream_kernel(SelectArgs a, RunConst rc) {
+__global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArgs a, RunConst rc) {
   constexpr int VN = Vec<T>::N;
   constexpr int CH = chunk_of<T>();
   constexpr bool ACCUM = MODE != kSelectOnly;

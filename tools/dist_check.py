@@ -1,0 +1,113 @@
+"""Multi-GPU parity check of the one-rank-per-GPU (NCCL) engine.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--n_g 200000] [--steps 20]
+
+Every rank runs Engine.rank() on its own GPU with gradients from the device
+generator keyed by (t, rank). Rank 0 also regenerates every rank's gradient
+on its own GPU (the generator is a pure function of (t, rank), so the bits are
+identical), feeds them to the fp32 oracle, and compares the records each step;
+at the end every rank's x / e / delta / k_t / topology are gathered (gloo) and
+compared with the oracle's replica of that rank. For N <= 2 the NCCL sum is
+order-independent, so x must match bit for bit; for N >= 3 x is checked to
+1e-6 relative (NCCL's reduction order differs from the reference's rank order).
+Exit code 0 on success.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n_g", type=int, default=200_003)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--d", type=float, default=0.01)
+    ap.add_argument("--skew", type=int, default=1)
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2402_13781_b200 import sparsim as S
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    kw = dict(n=world, n_g=args.n_g, n_b=max(16, 8 * world), d=args.d, seed=5, beta=1.05)
+    ids = [S.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    eng = S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype="f32"), rank, local, ids[0])
+    segs = O.skew_segments(args.n_g) if args.skew else None
+    src = S.SyntheticStream(S.StreamSpec(n_g=args.n_g, segments=segs, seed=5))
+    buf = torch.empty(args.n_g, device=f"cuda:{local}")
+    orc = O.OracleEngine(O.make_config(**kw), np.float32) if rank == 0 else None
+    tmp = torch.empty(args.n_g, device=f"cuda:{local}")
+    ok = True
+    for t in range(args.steps):
+        src.gradient(t, rank, buf, "f32", eng.stream())
+        torch.cuda.synchronize()
+        rec = eng.step([buf])
+        if rank == 0:
+            host = []
+            for r in range(world):
+                src.gradient(t, r, tmp, "f32", 0)
+                torch.cuda.synchronize()
+                host.append(tmp.cpu().numpy().copy())
+            orec = orc.step(host)
+            o = O.A.record_dict(orec)
+            for f in ("k_prime", "m_t", "c_t", "f_t", "delta", "density", "eps", "adjust_moves",
+                      "adjust_skips", "union_count"):
+                if getattr(rec, f) != o[f]:
+                    print(f"[rank0] t={t} {f}: gpu={getattr(rec, f)} oracle={o[f]}", flush=True)
+                    ok = False
+            if rec.k_rank != o["k_rank"]:
+                print(f"[rank0] t={t} k_rank {rec.k_rank} vs {o['k_rank']}", flush=True)
+                ok = False
+            if abs(rec.global_err - o["global_err"]) > 1e-6 * max(o["global_err"], 1e-300):
+                print(f"[rank0] t={t} global_err {rec.global_err} vs {o['global_err']}", flush=True)
+                ok = False
+            if not np.array_equal(eng.idx_global().astype(np.int64), orc.union()):
+                print(f"[rank0] t={t} union differs", flush=True)
+                ok = False
+    st = eng.state(0)
+    mine = {"x": eng.x(0), "e": eng.e(0), "delta": st.delta, "k_t": list(st.k_t[:world]),
+            "parts": st.topology.parts(), "sel": eng.selection(0)}
+    allst = [None] * world
+    dist.all_gather_object(allst, mine)
+    if rank == 0:
+        for r, m in enumerate(allst):
+            ost = orc.state(r)
+            if m["delta"] != ost.delta or m["k_t"] != list(ost.k_t[:world]) or \
+                    m["parts"] != ost.topology.parts():
+                print(f"[rank0] rank {r} control state differs", flush=True)
+                ok = False
+            if not np.array_equal(m["e"], orc.e(r)):
+                print(f"[rank0] rank {r} residual differs ({int(np.sum(m['e'] != orc.e(r)))})", flush=True)
+                ok = False
+            ox = orc.x(r)
+            if world <= 2:
+                same = np.array_equal(m["x"], ox)
+            else:
+                same = np.allclose(m["x"], ox, rtol=1e-6, atol=1e-7)
+            if not same:
+                print(f"[rank0] rank {r} x differs (max {np.max(np.abs(m['x'] - ox))})", flush=True)
+                ok = False
+            if not np.array_equal(m["sel"].astype(np.int64), orc.selection(r)):
+                print(f"[rank0] rank {r} selection differs", flush=True)
+                ok = False
+        print(f"dist_check world={world} n_g={args.n_g} steps={args.steps}: "
+              f"{'PASS' if ok else 'FAIL'} (last k'={rec.k_prime} f_t={rec.f_t:.3f})", flush=True)
+    flag = torch.tensor([1 if ok else 0])
+    dist.broadcast(flag, src=0)
+    dist.destroy_process_group()
+    sys.exit(0 if int(flag[0]) else 1)
+
+
+if __name__ == "__main__":
+    main()
