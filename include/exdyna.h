@@ -253,6 +253,11 @@ int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host,
                         int64_t cap_elems, int64_t* len);
 int exd_engine_copy_in(exd_engine* h, int32_t w, int32_t which, const void* host,
                        int64_t n_elems);
+/* Device address and current length of one of the EXD_VEC_* vectors (valid
+ * until exd_engine_destroy; contents valid after exd_engine_sync). The
+ * zero-copy form of Engine::workers() for device-side consumers. */
+int exd_engine_device_vector(exd_engine* h, int32_t w, int32_t which, void** ptr,
+                             int64_t* len);
 int exd_engine_kernel_stats(exd_engine* h, exd_kernel_stats* out);
 /* Turn per-kernel CUDA-event timing on/off (exd_options.profile_kernels).
  * With it on, an event sits between the stream and finish kernels, which

@@ -864,48 +864,73 @@ int exd_engine_get_state(exd_engine* h, int32_t w, exd_worker_state* out) {
   return EXD_OK;
 }
 
-int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host, int64_t cap,
-                        int64_t* len) {
+}  // extern "C"
+
+namespace {
+// (pointer, length, element size) of one EXD_VEC_* vector of worker w
+int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t* n_el,
+              size_t* es_out) {
   if (w < 0 || w >= (int)h->w.size()) return set_err(EXD_EINVAL, "worker out of range");
   if (int rc = sync_engine(h, nullptr)) return rc;
   Worker& wk = h->w[w];
-  const exd_record& rec = *h->w[w].rec_host;
-  int64_t n_el = 0;
+  const exd_record& rec = *wk.rec_host;
   size_t es = h->esz;
-  const void* src = nullptr;
   switch (which) {
-    case EXD_VEC_X: n_el = h->cfg.n_g; src = wk.x; break;
-    case EXD_VEC_E: n_el = h->cfg.n_g; src = wk.e; break;
+    case EXD_VEC_X: *n_el = h->cfg.n_g; *src = wk.x; break;
+    case EXD_VEC_E: *n_el = h->cfg.n_g; *src = wk.e; break;
     case EXD_VEC_IDX_GLOBAL:
-      n_el = h->has_record ? rec.k_prime : 0;
-      src = h->n > 1 ? (const void*)wk.idx_global : (const void*)wk.idx;
+      *n_el = h->has_record ? rec.k_prime : 0;
+      *src = h->n > 1 ? (const void*)wk.idx_global : (const void*)wk.idx;
       es = 4;
       break;
     case EXD_VEC_LOCAL_IDX:
     case EXD_VEC_LOCAL_VAL: {
       CountRec cr;
       CU(cudaMemcpy(&cr, wk.cnt, sizeof(cr), cudaMemcpyDeviceToHost));
-      n_el = h->has_record ? cr.k : 0;
-      src = which == EXD_VEC_LOCAL_IDX ? (const void*)wk.idx : wk.val;
+      *n_el = h->has_record ? cr.k : 0;
+      *src = which == EXD_VEC_LOCAL_IDX ? (const void*)wk.idx : wk.val;
       if (which == EXD_VEC_LOCAL_IDX) es = 4;
       break;
     }
     case EXD_VEC_BLOCK_COUNTS:
-      n_el = h->cfg.n_b;
-      src = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;  // parity of the last step
+      *n_el = h->cfg.n_b;
+      *src = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;  // parity of the last step
       es = 4;
       break;
     case EXD_VEC_SUM:
-      n_el = h->has_record ? rec.k_prime : 0;
-      src = h->n > 1 ? h->sum : wk.val;
+      *n_el = h->has_record ? rec.k_prime : 0;
+      *src = h->n > 1 ? h->sum : wk.val;
       break;
     default:
       return set_err(EXD_EINVAL, "unknown vector");
   }
+  *es_out = es;
+  return EXD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int exd_engine_copy_out(exd_engine* h, int32_t w, int32_t which, void* host, int64_t cap,
+                        int64_t* len) {
+  const void* src = nullptr;
+  int64_t n_el = 0;
+  size_t es = 0;
+  if (int rc = vector_of(h, w, which, &src, &n_el, &es)) return rc;
   if (len) *len = n_el;
   if (!host) return EXD_OK;
   if (n_el > cap) return set_err(EXD_EINVAL, "host buffer too small");
   if (n_el) CU(cudaMemcpy(host, src, es * (size_t)n_el, cudaMemcpyDeviceToHost));
+  return EXD_OK;
+}
+
+int exd_engine_device_vector(exd_engine* h, int32_t w, int32_t which, void** ptr, int64_t* len) {
+  const void* src = nullptr;
+  int64_t n_el = 0;
+  size_t es = 0;
+  if (int rc = vector_of(h, w, which, &src, &n_el, &es)) return rc;
+  if (ptr) *ptr = const_cast<void*>(src);
+  if (len) *len = n_el;
   return EXD_OK;
 }
 

@@ -415,6 +415,23 @@ class Engine:
     def reduced(self, w=0):
         return self._copy(w, A.EXD_VEC_SUM, self.np_dtype)
 
+    def device_view(self, w, which):
+        """Zero-copy torch view of x / e / idx_global / ... of worker w (device
+        memory owned by the engine; valid until close())."""
+        import torch
+        code = {"x": A.EXD_VEC_X, "e": A.EXD_VEC_E, "idx_global": A.EXD_VEC_IDX_GLOBAL,
+                "selection": A.EXD_VEC_LOCAL_IDX, "selected_values": A.EXD_VEC_LOCAL_VAL,
+                "block_counts": A.EXD_VEC_BLOCK_COUNTS, "reduced": A.EXD_VEC_SUM}[which]
+        ptr, n = C.c_void_p(), C.c_int64()
+        check(self.L.exd_engine_device_vector(self.h, w, code, C.byref(ptr), C.byref(n)))
+        int_vec = code in (A.EXD_VEC_IDX_GLOBAL, A.EXD_VEC_LOCAL_IDX, A.EXD_VEC_BLOCK_COUNTS)
+        typestr = "<i4" if int_vec else ("<f8" if self.esize == 8 else "<f4")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": typestr,
+                                        "data": (ptr.value or 0, False), "version": 3}
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
     def write(self, w, which, arr):
         """mutable_workers() (engine.hpp:72-74): overwrite x or e of worker w."""
         a = np.ascontiguousarray(arr, dtype=self.np_dtype)
