@@ -48,7 +48,8 @@ def workload(n):
             "n_g": N_G, "d": DENSITY, "k": round(DENSITY * N_G), "n_b": N_B, "workers": n,
             "alpha": 1.25, "beta": 1.25, "gamma": 0.02, "min_blk": 2, "blk_move": 1,
             "delta0": "auto (t=0 quantile)", "stream": "default 4-segment Laplace, seed 7",
-            "l2": "flushed before every timed step (2x L2 buffer written, then read back)", "parallelism": f"dp{n}"}
+            "l2": "flushed before every timed step (2x L2 buffer written, then read back)", "parallelism": f"dp{n}",
+            "sync": "single GPU" if n == 1 else None}
 
 
 # ------------------------------------------------------------------ clocks --
@@ -204,7 +205,7 @@ def run_ours(args):
         dist.init_process_group("gloo")  # control plane only; the data path is NCCL in C++
     kw = cfg_kw(n)
     opt = S.EngineOptions(dtype="f32", profile_kernels=False, verify_replication=False,
-                          record_loss=False)
+                          record_loss=False, sync=args.sync)
     if n == 1:
         eng = S.Engine(S.SparsifierConfig(**kw), opt, device=local)
     else:
@@ -349,10 +350,14 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    cfg_line = workload(n)
+    if n > 1:
+        cfg_line["sync"] = ("NVLink peer-memory kernels (no host wait)" if eng.sync_mode() == "p2p"
+                            else "NCCL all-gather/all-reduce + one host wait")
     line = {
         "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(n),
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg_line,
         "selection_hbm_gbs": achieved,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -377,6 +382,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N > 1: NVLink peer-memory sync (auto/p2p) or the NCCL chain")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

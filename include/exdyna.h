@@ -82,7 +82,15 @@ typedef struct exd_options {
   int32_t record_loss;           /* accepted; synthetic streams have no loss */
   int32_t dtype;                 /* EXD_F32 (default) or EXD_F64 (strict oracle mode) */
   int32_t profile_kernels;       /* time the fused select kernel with CUDA events */
+  int32_t sync_mode;             /* one-rank-per-GPU sync: EXD_SYNC_* */
 } exd_options;
+
+/* exd_options.sync_mode (exd_engine_create_rank only) */
+enum {
+  EXD_SYNC_AUTO = 0,   /* NVLink peer memory when every peer is P2P-reachable, else NCCL */
+  EXD_SYNC_NCCL = 1,   /* count all-gather, host wait, padded index all-gather, all-reduce */
+  EXD_SYNC_P2P = 2     /* peer-memory kernels, no host in the loop (fails if unavailable) */
+};
 
 /* PartitionTopology, types.hpp:36-46 */
 typedef struct exd_topology {
@@ -231,6 +239,8 @@ void exd_engine_destroy(exd_engine* h);
 int32_t exd_engine_local_workers(const exd_engine* h);
 int32_t exd_engine_first_rank(const exd_engine* h);
 int64_t exd_engine_iteration(const exd_engine* h);
+/* collective path in use: EXD_SYNC_P2P or EXD_SYNC_NCCL (-1: in-process workers) */
+int32_t exd_engine_sync_mode(const exd_engine* h);
 /* CUDA stream of local worker w (cudaStream_t as void*) */
 void* exd_engine_stream(const exd_engine* h, int32_t w);
 

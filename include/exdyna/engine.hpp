@@ -10,9 +10,9 @@
 //   sparsim::EngineError       -> exdyna::EngineError        (engine.hpp:47-50)
 //
 // Differences a caller sees: gradients are DEVICE buffers (one per local
-// worker) instead of a host GradientSource callback — HostGradientSource below
-// adapts a host source; the engine works in fp32 (Precision::F32) or in the
-// reference's fp64 (Precision::F64).
+// worker) instead of a host GradientSource callback (step_host() takes the
+// host buffers such a source fills); the engine works in fp32
+// (Precision::F32) or in the reference's fp64 (Precision::F64).
 #pragma once
 
 #include <cstring>
@@ -110,6 +110,7 @@ struct EngineOptions {
   bool verify_conservation = false;
   Precision precision = Precision::F32;
   bool profile_kernels = false;
+  int sync_mode = EXD_SYNC_AUTO;
 
   exd_options to_c() const {
     exd_options o{};
@@ -121,6 +122,7 @@ struct EngineOptions {
     o.record_loss = 0;
     o.dtype = static_cast<int32_t>(precision);
     o.profile_kernels = profile_kernels;
+    o.sync_mode = sync_mode;
     return o;
   }
 };

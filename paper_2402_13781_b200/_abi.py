@@ -11,6 +11,7 @@ NCCL_ID_BYTES = 128
 
 EXD_OK, EXD_EINVAL, EXD_EINVARIANT, EXD_ECUDA, EXD_ENCCL, EXD_ENOMEM, EXD_EUNSUPPORTED = range(7)
 EXD_F32, EXD_F64 = 0, 1
+EXD_SYNC_AUTO, EXD_SYNC_NCCL, EXD_SYNC_P2P = 0, 1, 2
 EXD_SPARSIFIER_EXDYNA, EXD_SPARSIFIER_TOPK, EXD_SPARSIFIER_CLTK, EXD_SPARSIFIER_HARD_THRESHOLD = range(4)
 (EXD_VEC_X, EXD_VEC_E, EXD_VEC_IDX_GLOBAL, EXD_VEC_LOCAL_IDX, EXD_VEC_LOCAL_VAL,
  EXD_VEC_BLOCK_COUNTS, EXD_VEC_SUM) = range(7)
@@ -32,7 +33,7 @@ class exd_options(C.Structure):
         ("sparsifier", i32), ("static_partitions", i32), ("fixed_delta", f64),
         ("parallel_workers", i32), ("verify_replication", i32),
         ("verify_conservation", i32), ("record_loss", i32), ("dtype", i32),
-        ("profile_kernels", i32),
+        ("profile_kernels", i32), ("sync_mode", i32),
     ]
 
 

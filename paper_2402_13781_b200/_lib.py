@@ -78,6 +78,7 @@ def lib():
     _sig(L, "exd_engine_local_workers", C.c_int32, [P])
     _sig(L, "exd_engine_first_rank", C.c_int32, [P])
     _sig(L, "exd_engine_iteration", C.c_int64, [P])
+    _sig(L, "exd_engine_sync_mode", C.c_int32, [P])
     _sig(L, "exd_engine_stream", P, [P, C.c_int32])
     _sig(L, "exd_engine_step", C.c_int, [P, C.POINTER(P), C.POINTER(A.exd_record)])
     _sig(L, "exd_engine_step_async", C.c_int, [P, C.POINTER(P)])
@@ -116,6 +117,7 @@ EXPORTED = [
     "exd_gather_stats_of", "exd_initial_threshold_device", "exd_synthetic_gradient",
     "exd_engine_create", "exd_nccl_unique_id", "exd_engine_create_rank", "exd_engine_destroy",
     "exd_engine_local_workers", "exd_engine_first_rank", "exd_engine_iteration",
+    "exd_engine_sync_mode",
     "exd_engine_stream", "exd_engine_step", "exd_engine_step_async", "exd_engine_sync",
     "exd_engine_step_host", "exd_engine_get_state", "exd_engine_copy_out", "exd_engine_copy_in",
     "exd_engine_device_vector",

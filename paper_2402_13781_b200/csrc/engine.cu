@@ -218,6 +218,18 @@ struct exd_engine {
   int64_t verify_t = -1;
   // dist
   ncclComm_t comm = nullptr;
+  // NVLink peer-memory sync (f1)
+  bool p2p = false;
+  void* region = nullptr;             // exported inbox: flags[n] | lists[n] | contrib[2]
+  std::vector<void*> peer_regions;    // opened IPC mappings (nullptr for self)
+  PeerFlags* inbox = nullptr;         // own inbox flag slots (local)
+  PeerFlags** d_slot = nullptr;       // [n] my slot in every rank's inbox
+  const int32_t** d_p2p_lists = nullptr;  // [n] lists to read (own idx / inbox slots)
+  int32_t** d_push = nullptr;         // [n-1] my list slot in every peer's inbox
+  void** d_contrib = nullptr;         // [2][n]
+  unsigned int* p2p_err = nullptr;    // pinned host copy
+  unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
+  unsigned long long* p2p_gate = nullptr;  // [2] local gate words
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
   // profiling
@@ -369,7 +381,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
       contribs[i] = h->w[i].contrib;
     }
     CU(cudaMalloc((void**)&h->d_lists, sizeof(void*) * n));
-    CU(cudaMemcpy(h->d_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_p2p_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
     CU(cudaMalloc((void**)&h->d_contribs, sizeof(void*) * n));
     CU(cudaMemcpy(h->d_contribs, contribs.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
   }
@@ -381,6 +393,26 @@ void teardown(exd_engine* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->p2p && h->comm) {
+    // barrier: no peer may still be reading our region when it is freed
+    float* one = nullptr;
+    if (cudaMalloc((void**)&one, sizeof(float)) == cudaSuccess) {
+      cudaMemset(one, 0, sizeof(float));
+      nccl().AllReduce(one, one, 1, ncclFloat32, ncclSum, h->comm, h->stream);
+      cudaStreamSynchronize(h->stream);
+      cudaFree(one);
+    }
+  }
+  for (void* p : h->peer_regions)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (h->p2p) cudaFree(h->region);
+  cudaFree(h->d_slot);
+  cudaFree(h->d_p2p_lists);
+  cudaFree(h->d_push);
+  cudaFree(h->d_contrib);
+  cudaFreeHost(h->p2p_err);
+  cudaFree(h->p2p_err_dev);
+  cudaFree(h->p2p_gate);
   for (auto& wk : h->w) {
     cudaFree(wk.x);
     cudaFree(wk.e);
@@ -415,6 +447,106 @@ void teardown(exd_engine* h) {
   for (auto& ev : h->free_ev) cudaEventDestroy(ev);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+// f1: export one IPC region per rank (flags | selection list | two contribution
+// buffers), exchange the handles with one NCCL all-gather, map every peer.
+// Returns EXD_OK with h->p2p == false when the peers are not P2P-reachable
+// and the caller asked for EXD_SYNC_AUTO.
+int setup_p2p(exd_engine* h) {
+  const int n = h->n, me = h->w[0].rank;
+  // can this device reach every other device directly? (decided collectively:
+  // every rank must take the same path)
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  int ok_local = 1;
+  for (int d = 0; d < ndev; ++d) {
+    if (d == h->device) continue;
+    int can = 0;
+    CU(cudaDeviceCanAccessPeer(&can, h->device, d));
+    ok_local &= can;
+  }
+  int* d_ok = nullptr;
+  CU(cudaMalloc((void**)&d_ok, sizeof(int)));
+  CU(cudaMemcpy(d_ok, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
+  NC(nccl().AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, h->comm, h->stream));
+  int ok_all = 0;
+  CU(cudaMemcpyAsync(&ok_all, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  cudaFree(d_ok);
+  if (!ok_all) {
+    if (h->opt.sync_mode == EXD_SYNC_P2P)
+      return set_err(EXD_EUNSUPPORTED, "EXD_SYNC_P2P: some peers are not P2P-reachable");
+    return EXD_OK;
+  }
+  // inbox layout: flags[n] | lists[n][cap_part] | contrib[2][n_g]
+  const size_t flags_b = ((sizeof(PeerFlags) * (size_t)n) + 255) & ~(size_t)255;
+  const size_t list_b = ((4 * (size_t)h->cap_part) + 255) & ~(size_t)255;
+  const size_t con_b = ((h->esz * (size_t)h->cfg.n_g) + 255) & ~(size_t)255;
+  const size_t off_lists = flags_b, off_c0 = off_lists + list_b * (size_t)n, off_c1 = off_c0 + con_b;
+  const size_t total = off_c1 + con_b;
+  CU(cudaMalloc(&h->region, total));
+  CU(cudaMemset(h->region, 0, flags_b));
+  h->inbox = static_cast<PeerFlags*>(h->region);
+  Worker& wk = h->w[0];
+  cudaIpcMemHandle_t mine;
+  CU(cudaIpcGetMemHandle(&mine, h->region));
+  char* d_handles = nullptr;
+  CU(cudaMalloc((void**)&d_handles, sizeof(cudaIpcMemHandle_t) * n));
+  CU(cudaMemcpy(d_handles + sizeof(cudaIpcMemHandle_t) * me, &mine, sizeof(mine),
+                cudaMemcpyHostToDevice));
+  NC(nccl().AllGather(d_handles + sizeof(cudaIpcMemHandle_t) * me, d_handles,
+                      sizeof(cudaIpcMemHandle_t), ncclUint8, h->comm, h->stream));
+  std::vector<cudaIpcMemHandle_t> all(n);
+  CU(cudaMemcpyAsync(all.data(), d_handles, sizeof(cudaIpcMemHandle_t) * n,
+                     cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  cudaFree(d_handles);
+  h->peer_regions.assign(n, nullptr);
+  std::vector<char*> base(n);
+  for (int r = 0; r < n; ++r) {
+    if (r == me) {
+      base[r] = static_cast<char*>(h->region);
+      continue;
+    }
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+    h->peer_regions[r] = p;
+    base[r] = static_cast<char*>(p);
+  }
+  std::vector<PeerFlags*> slot(n);
+  std::vector<const int32_t*> lists(n);
+  std::vector<int32_t*> push;
+  std::vector<void*> con(2 * n);
+  char* own = static_cast<char*>(h->region);
+  for (int r = 0; r < n; ++r) {
+    slot[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
+    lists[r] = r == me ? wk.idx : reinterpret_cast<const int32_t*>(own + off_lists + list_b * r);
+    if (r != me) push.push_back(reinterpret_cast<int32_t*>(base[r] + off_lists + list_b * me));
+    con[r] = base[r] + off_c0;
+    con[n + r] = base[r] + off_c1;
+  }
+  CU(cudaMalloc((void**)&h->d_slot, sizeof(void*) * n));
+  CU(cudaMalloc((void**)&h->d_p2p_lists, sizeof(void*) * n));
+  CU(cudaMalloc((void**)&h->d_push, sizeof(void*) * (n > 1 ? n - 1 : 1)));
+  CU(cudaMalloc((void**)&h->d_contrib, sizeof(void*) * 2 * n));
+  CU(cudaMemcpy(h->d_slot, slot.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_p2p_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_push, push.data(), sizeof(void*) * push.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_contrib, con.data(), sizeof(void*) * 2 * n, cudaMemcpyHostToDevice));
+  CU(cudaHostAlloc((void**)&h->p2p_err, sizeof(unsigned int), cudaHostAllocDefault));
+  *h->p2p_err = 0;
+  if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
+  if (int r2 = alloc_zero((void**)&h->p2p_gate, 2 * sizeof(unsigned long long))) return r2;
+  // barrier: every rank has mapped every peer before anyone steps
+  int* d_b = nullptr;
+  CU(cudaMalloc((void**)&d_b, sizeof(int)));
+  CU(cudaMemset(d_b, 0, sizeof(int)));
+  NC(nccl().AllReduce(d_b, d_b, 1, ncclInt32, ncclSum, h->comm, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  cudaFree(d_b);
+  h->p2p = true;
+  return EXD_OK;
 }
 
 // K1 (stream) and, unless accumulate-only, K2 (finish); CUDA events around
@@ -467,6 +599,8 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.tile_base = 0;
   a.num_tiles = (int32_t)h->tiles;
   a.t = h->t;
+  a.push_idx = h->p2p ? h->d_push : nullptr;
+  a.npush = h->p2p ? h->n - 1 : 0;
   return a;
 }
 
@@ -518,7 +652,31 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   }
 
   if (n > 1) {
-    if (h->dist) {
+    if (h->dist && h->p2p) {
+      // f1: peer-memory sync, no host wait, no NCCL
+      Worker& wk = h->w[0];
+      P2PArgs pa{};
+      pa.inbox = h->inbox;
+      pa.peer_slot = h->d_slot;
+      pa.lists = h->d_p2p_lists;
+      pa.contrib = h->d_contrib + (h->t & 1) * n;
+      pa.own_val = wk.val;
+      pa.e = wk.e;
+      pa.x = wk.x;
+      pa.idx_global = wk.idx_global;
+      pa.sum = h->sum;
+      pa.counts_all = h->counts_all;
+      pa.own_cnt = wk.cnt;
+      pa.ctrl = wk.ctrl;
+      pa.rec = wk.rec_dev + (h->t % kRecRing);
+      pa.epoch = (unsigned long long)h->t + 1;
+      pa.err = h->p2p_err_dev;
+      pa.gate = h->p2p_gate;
+      pa.me = wk.rank;
+      CU(launch_p2p_union(pa, wk.rc, h->stream));
+      CU(launch_p2p_reduce(pa, wk.rc, h->stream));
+      h->stats.kernel_launches += 2;
+    } else if (h->dist) {
       Worker& wk = h->w[0];
       NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));
       CU(cudaMemcpyAsync(h->counts_host, h->counts_all, sizeof(CountRec) * n,
@@ -626,6 +784,11 @@ int sync_engine(exd_engine* h, exd_record* out) {
     h->free_ev.push_back(p.c);
   }
   h->pending.clear();
+  if (h->p2p) {
+    CU(cudaMemcpy(h->p2p_err, h->p2p_err_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    if (*h->p2p_err)
+      return set_err(EXD_ENCCL, "peer-memory sync: a peer did not arrive within 20 s");
+  }
   if (*h->verify_flag) {
     const uint32_t f = *h->verify_flag;
     const char* field = (f & 1) ? "delta" : (f & 2) ? "k_t" : (f & 4) ? "topology" : "x";
@@ -799,6 +962,7 @@ int exd_engine_create_rank(const exd_config* cfg, const exd_options* opt, int32_
       cudaSetDevice(device);
       ncclResult_t r = nc.CommInitRank(&h->comm, cfg->n, id, rank);
       if (r != ncclSuccess) rc = set_err(EXD_ENCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
+      if (!rc && opt->sync_mode != EXD_SYNC_NCCL) rc = setup_p2p(h);
     }
   }
   if (rc) {
@@ -820,6 +984,9 @@ void exd_engine_destroy(exd_engine* h) {
 int32_t exd_engine_local_workers(const exd_engine* h) { return (int32_t)h->w.size(); }
 int32_t exd_engine_first_rank(const exd_engine* h) { return h->w.empty() ? 0 : h->w[0].rank; }
 int64_t exd_engine_iteration(const exd_engine* h) { return h->t; }
+int32_t exd_engine_sync_mode(const exd_engine* h) {
+  return !h->dist ? -1 : (h->p2p ? EXD_SYNC_P2P : EXD_SYNC_NCCL);
+}
 void* exd_engine_stream(const exd_engine* h, int32_t) { return (void*)h->stream; }
 
 int exd_engine_step_async(exd_engine* h, const void* const* grads_dev) {

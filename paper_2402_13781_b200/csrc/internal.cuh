@@ -79,6 +79,8 @@ struct SelectArgs {
   int32_t tile_base;        // first tile covered by the stream launch
   int32_t num_tiles;        // tiles covered by the stream launch
   int64_t t;                // the step these kernels run (selects plan[t & 1])
+  int32_t* const* push_idx;  // P2P: [n] my list slot in every peer's inbox (nullptr: none)
+  int32_t npush;
 };
 
 constexpr int kMaxCtas = 2048;
@@ -105,6 +107,39 @@ struct FinalizeArgs {
   exd_record* rec;              // record (mapped host memory)
 };
 
+// ---- NVLink peer-memory sync (one rank per GPU, no host in the loop) --------
+// Each rank exports one IPC region = its INBOX: one flag slot per source rank,
+// one index-list slot per source rank, and its own contributions (two step-
+// parity buffers). Senders PUSH into the receiver's inbox (posted NVLink
+// stores); receivers poll their own local memory. Epochs are t + 1.
+struct PeerFlags {                   // inbox[src] on the receiver
+  unsigned long long count_epoch;    // src's {k, norm2} and index list of step epoch-1 arrived
+  int64_t k;
+  double norm2;
+  unsigned long long contrib_epoch;  // src's contributions of step epoch-1 are readable
+  unsigned long long pad[12];        // 128 B: one slot per line
+};
+
+struct P2PArgs {
+  PeerFlags* inbox;                  // [n] own inbox flag slots (local)
+  PeerFlags* const* peer_slot;       // [n] my slot in every rank's inbox (remote; own = local)
+  const int32_t* const* lists;       // [n] index lists: own `idx` or inbox list slot (local)
+  void* const* contrib;              // [n] contribution buffers of this step's parity (remote; own local)
+  const void* own_val;               // own selected values (T)
+  void* e;
+  void* x;
+  int32_t* idx_global;               // [k'] union
+  void* sum;                         // [k'] all-reduced values (T)
+  CountRec* counts_all;              // [n] local copy of the gathered counts
+  const CountRec* own_cnt;           // the finish kernel's {k_i, ||e||^2}
+  Ctrl* ctrl;
+  exd_record* rec;
+  unsigned long long epoch;          // t + 1
+  unsigned int* err;                 // set on a peer timeout (device memory)
+  unsigned long long* gate;          // [2] local gates: count / contrib epoch seen by block 0
+  int32_t me;
+};
+
 // kernel launchers (kernels.cu)
 int tile_elems(int dtype);
 int64_t num_tiles(int64_t n_g, int dtype);
@@ -123,6 +158,8 @@ cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void
                                       const void* xw, int64_t n_g, int dtype, int32_t w,
                                       uint32_t* flag, cudaStream_t s);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
+cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s);
+cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
 

@@ -522,6 +522,8 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
 
   Ctrl* ctrl = a.ctrl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // P2P: let the union kernel launch early (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // block 0 is the epilogue CTA (dispatched first, so its control-block
   // prefetch overlaps the stream kernel's tail); blocks 1..G copy
   const int G = gridDim.x - 1, r = (int)blockIdx.x - 1;
@@ -665,6 +667,8 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
         if (i < btot) {
           idx[running + i] = jj[q];
           val[running + i] = vv[q];
+          // P2P: push the list into every peer's inbox (posted NVLink stores)
+          for (int pr = 0; pr < a.npush; ++pr) a.push_idx[pr][running + i] = jj[q];
           if (FUSED) x[jj[q]] = apply_update<T>(xx[q], vv[q], rc.n);
         }
       }
@@ -801,6 +805,233 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a, RunConst 
     __syncthreads();
     control_epilogue_cta(a.ctrl, a.counts, rc, a.rec);
   }
+}
+
+// ---- f1: NVLink peer-memory sync -------------------------
+// Replaces the NCCL chain (count all-gather -> host wait -> padded index
+// all-gather -> all-reduce) with kernels that talk over NVLink directly, with
+// no host in the loop and no padding:
+//   finish      (already running) also PUSHES this rank's ascending index list
+//               into its slot of every peer's inbox (posted NVLink stores).
+//   p2p_union   publishes {k_i, ||e||^2} + an epoch into every peer's inbox,
+//               waits on its OWN inbox (local polling), builds the union in
+//               partition order from the (now local) lists, gathers this rank's
+//               contributions, clears e at the union.
+//   p2p_reduce  publishes "contributions ready", waits, sums the contributions
+//               in RANK ORDER straight from the peers' buffers (bit-identical to
+//               all_reduce_sum, collectives.cpp:59-70, for every n), x -= g/n,
+//               control epilogue.
+// Buffer reuse is safe without extra handshakes: a rank overwrites its list
+// slot / count in a peer's inbox only in step t+1, after its own p2p_reduce(t)
+// saw that peer's contrib epoch t+1 (published when the peer had finished
+// p2p_union(t)); contributions are double buffered by step parity.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_i64(int64_t* p, int64_t v) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block 0 polls its LOCAL inbox (the senders pushed their epochs there), one
+// system-scope acquire fence once everyone is in, then opens a local gate word
+// for the other blocks. Gives up after 20 s (sets `err`) so a dead peer cannot
+// hang the GPU. Call from thread 0; returns false on timeout.
+__device__ bool wait_inbox(const PeerFlags* inbox, int n, bool contrib, unsigned long long epoch,
+                           unsigned long long* gate, unsigned int* err) {
+  const unsigned long long t0 = gtime_ns();
+  if (blockIdx.x == 0) {
+    for (int r = 0; r < n; ++r) {
+      const unsigned long long* w = contrib ? &inbox[r].contrib_epoch : &inbox[r].count_epoch;
+      unsigned spins = 0;
+      while (ld_relaxed_sys(w) < epoch) {
+        if ((++spins & 255u) == 0 && gtime_ns() - t0 > 20000000000ull) {
+          atomicExch(err, 1u);
+          st_release_gpu(gate, ~0ull);  // release the other blocks, they see err
+          return false;
+        }
+        __nanosleep(20);
+      }
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    st_release_gpu(gate, epoch);
+    return true;
+  }
+  unsigned spins = 0;
+  unsigned long long gv;
+  while ((gv = ld_acquire_gpu(gate)) < epoch) {
+    if ((++spins & 255u) == 0 && gtime_ns() - t0 > 21000000000ull) {
+      atomicExch(err, 1u);
+      return false;
+    }
+    __nanosleep(20);
+  }
+  return gv != ~0ull && *(volatile unsigned int*)err == 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) {
+  __shared__ int64_t s_off[EXD_MAX_WORKERS + 1];
+  __shared__ int32_t s_rank[EXD_MAX_WORKERS];
+  __shared__ bool s_ok;
+  const int n = rc.n, tid = threadIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the finish kernel's list pushes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (blockIdx.x == 0) PROBE(20);
+  if (blockIdx.x == 0 && tid < n) {
+    // announce {k_i, ||e||^2}: the pushed list is complete (previous kernel);
+    // one system fence orders the payload before the epoch (a release store
+    // would add a second one: profiles/p2p_latency_r01.txt)
+    PeerFlags* slot = a.peer_slot[tid];
+    st_relaxed_sys_i64(&slot->k, a.own_cnt->k);
+    st_relaxed_sys_f64(&slot->norm2, a.own_cnt->norm2);
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    st_relaxed_sys(&slot->count_epoch, a.epoch);
+  }
+  if (tid == 0) s_ok = wait_inbox(a.inbox, n, false, a.epoch, &a.gate[0], a.err);
+  __syncthreads();
+  if (blockIdx.x == 0) PROBE(21);
+  if (!s_ok) return;
+  if (tid == 0) {
+    const int64_t tm = mod_floor(a.ctrl->t, n);
+    int64_t off = 0;
+    for (int p = 0; p < n; ++p) {
+      const int r = (int)mod_floor(p - tm, n);
+      s_rank[p] = r;
+      s_off[p] = off;
+      off += __ldcg(&a.inbox[r].k);
+    }
+    s_off[n] = off;
+  }
+  if (blockIdx.x == 0 && tid < n) {
+    a.counts_all[tid].k = __ldcg(&a.inbox[tid].k);
+    a.counts_all[tid].norm2 = __ldcg(&a.inbox[tid].norm2);
+  }
+  __syncthreads();
+  const int64_t kp = s_off[n];
+  T* e = static_cast<T*>(a.e);
+  T* c = static_cast<T*>(a.contrib[a.me]);
+  const T* own = static_cast<const T*>(a.own_val);
+  const T* xx = static_cast<const T*>(a.x);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // 4 entries per thread in flight: list reads, then residual reads, then writes
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 4 * stride) {
+    int32_t j[4];
+    int r4[4];
+    int64_t loc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t pos = p0 + q * stride;
+      r4[q] = -1;
+      if (pos < kp) {
+        int p = 0;
+        while (p + 1 < n && s_off[p + 1] <= pos) ++p;
+        r4[q] = s_rank[p];
+        loc[q] = pos - s_off[p];
+        j[q] = __ldcg(&a.lists[r4[q]][loc[q]]);  // local: own list or pushed inbox slot
+      }
+    }
+    T v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (r4[q] < 0) continue;
+      v[q] = r4[q] == a.me ? own[loc[q]] : e[j[q]];  // own residual already cleared
+      // the reduce kernel read-modify-writes x[j]: pull the line into L2 now
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(xx + j[q]));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (r4[q] < 0) continue;
+      const int64_t pos = p0 + q * stride;
+      a.idx_global[pos] = j[q];
+      c[pos] = v[q];
+      if (r4[q] != a.me) e[j[q]] = T(0);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) p2p_reduce_kernel(P2PArgs a, RunConst rc) {
+  __shared__ bool s_ok;
+  const int n = rc.n, tid = threadIdx.x;
+  const int G = gridDim.x - 1;  // last block: control epilogue (needs only the counts)
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // our contributions are complete
+  if ((int)blockIdx.x == G) {
+    control_epilogue_cta(a.ctrl, a.counts_all, rc, a.rec);
+    PROBE(24);
+    return;
+  }
+  if (blockIdx.x == 0) PROBE(22);
+  if (blockIdx.x == 0 && tid < n) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");  // our contributions (previous kernel)
+    st_relaxed_sys(&a.peer_slot[tid]->contrib_epoch, a.epoch);
+  }
+  if (tid == 0) s_ok = wait_inbox(a.inbox, n, true, a.epoch, &a.gate[1], a.err);
+  __syncthreads();
+  if (blockIdx.x == 0) PROBE(23);
+  if (!s_ok) return;
+  int64_t kp = 0;
+  for (int r = 0; r < n; ++r) kp += a.counts_all[r].k;
+  T* x = static_cast<T*>(a.x);
+  T* g = static_cast<T*>(a.sum);
+  const int64_t stride = (int64_t)G * blockDim.x;
+  const int nn = n < 8 ? n : 8;
+  // 2 entries per thread in flight: every peer's contribution for both, then x
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 2 * stride) {
+    T v[2][8];
+    int32_t j[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t pos = p0 + q * stride;
+      if (pos < kp) {
+        for (int r = 0; r < nn; ++r) v[q][r] = __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
+        j[q] = a.idx_global[pos];
+      }
+    }
+    T xv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (p0 + q * stride < kp) xv[q] = x[j[q]];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t pos = p0 + q * stride;
+      if (pos >= kp) continue;
+      T s = v[q][0];  // rank order, as all_reduce_sum (collectives.cpp:62-68)
+      for (int r = 1; r < nn; ++r) s += v[q][r];
+      for (int r = 8; r < n; ++r) s += __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
+      g[pos] = s;
+      x[j[q]] = apply_update<T>(xv[q], s, n);
+    }
+  }
+  if (blockIdx.x == 0) PROBE(25);
 }
 
 // ---- delta0 broadcast into every worker's control block ---------------------
@@ -1052,6 +1283,44 @@ cudaError_t launch_finalize(FinalizeArgs a, RunConst rc, cudaStream_t s) {
   if (rc.dtype == EXD_F64) finalize_kernel<double><<<blocks, 256, 0, s>>>(a, rc);
   else finalize_kernel<float><<<blocks, 256, 0, s>>>(a, rc);
   return cudaGetLastError();
+}
+
+// every block's thread 0 polls the peers' flags: keep the grid at two CTAs
+// per SM (k' <= n_g entries are covered by the grid-stride loops)
+static int p2p_blocks() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return 2 * sms;
+}
+
+// programmatic launch: overlap each launch with the previous kernel's tail;
+// the kernels start with griddepcontrol.wait
+template <typename K>
+static cudaError_t launch_pdl(K kernel, int blocks, cudaStream_t s, const P2PArgs& a,
+                              const RunConst& rc) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a, rc);
+}
+
+cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s) {
+  const int blocks = p2p_blocks();
+  if (rc.dtype == EXD_F64) return launch_pdl(p2p_union_kernel<double>, blocks, s, a, rc);
+  return launch_pdl(p2p_union_kernel<float>, blocks, s, a, rc);
+}
+
+cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s) {
+  const int blocks = p2p_blocks() + 1;
+  if (rc.dtype == EXD_F64) return launch_pdl(p2p_reduce_kernel<double>, blocks, s, a, rc);
+  return launch_pdl(p2p_reduce_kernel<float>, blocks, s, a, rc);
 }
 
 cudaError_t launch_set_delta(Ctrl* const* ctrls, int nctrl, const void* bits, int dtype,

@@ -1,0 +1,40 @@
+"""Experiment: per-step timeline of the one-rank-per-GPU step (torchrun).
+EXD_LIB=paper_2402_13781_b200/lib/libexdyna_probe.so torchrun --nproc-per-node 2 tools/probe_dist.py --sync p2p
+"""
+import argparse, ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ap = argparse.ArgumentParser(); ap.add_argument("--sync", default="p2p"); ap.add_argument("--flush", type=int, default=0)
+a = ap.parse_args()
+import torch, torch.distributed as dist
+from paper_2402_13781_b200 import sparsim as S
+from paper_2402_13781_b200._lib import lib
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank)); torch.cuda.set_device(local)
+dist.init_process_group("gloo")
+ids = [S.nccl_unique_id() if rank == 0 else None]; dist.broadcast_object_list(ids, src=0)
+n_g = 11_200_000
+eng = S.Engine.rank(S.SparsifierConfig(n=world, n_g=n_g, n_b=256, d=0.01, seed=7),
+                    S.EngineOptions(sync=a.sync, verify_replication=False), rank, local, ids[0])
+src = S.SyntheticStream(S.StreamSpec(n_g=n_g, seed=7))
+bufs = [torch.empty(n_g, device=f"cuda:{local}") for _ in range(2)]
+for i, b in enumerate(bufs): src.gradient(i, rank, b, "f32", eng.stream())
+torch.cuda.synchronize()
+for i in range(300): eng.step_async([bufs[i % 2]])
+eng.sync(); dist.barrier()
+xs = torch.cuda.ExternalStream(eng.stream())
+evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+for i in range(50):
+    if a.flush: S.flush_l2(local, eng.stream())
+    evs[i][0].record(xs); eng.step_async([bufs[i % 2]]); evs[i][1].record(xs)
+eng.sync()
+us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in evs)
+out = f"rank {rank} sync={eng.sync_mode()} flush={a.flush}: step median {us[25]:.1f} us min {us[0]:.1f} max {us[-1]:.1f}"
+L = lib()
+if hasattr(L, "exd_debug_probe"):
+    L.exd_debug_probe.argtypes = [C.POINTER(C.c_uint64)]
+    buf = (C.c_uint64 * 64)(); L.exd_debug_probe(buf)
+    t0 = buf[16]
+    names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "gather", 21: "gather_waited", 22: "reduce", 23: "reduce_waited", 24: "reduce_epi_end", 25: "reduce_b0_end"}
+    out += "  | " + "  ".join(f"{v}={(buf[k]-t0)/1e3:.1f}" for k, v in sorted(names.items(), key=lambda kv: buf[kv[0]]) if buf[k])
+print(out, flush=True)
+dist.barrier(); dist.destroy_process_group()
