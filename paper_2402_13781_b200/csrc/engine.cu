@@ -175,8 +175,7 @@ struct Worker {
   int32_t* idx = nullptr;
   void* val = nullptr;
   int32_t* blk = nullptr;             // 2 x n_b (double-buffered by step parity)
-  int32_t* stage_idx = nullptr;       // warp-chunk staging of the compaction
-  void* stage_val = nullptr;
+  void* stage = nullptr;              // warp-chunk staging of the compaction ((idx, val) pairs)
   int32_t* chunk_count = nullptr;
   int32_t* tile_count = nullptr;
   double* cta_norm = nullptr;
@@ -334,8 +333,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero(&wk.val, h->esz * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero((void**)&wk.blk, 4 * 2 * (size_t)cfg.n_b)) return r;
     const size_t stage_cap = (size_t)h->cap_part + 2 * (size_t)h->tile;
-    if (int r = alloc_zero((void**)&wk.stage_idx, 4 * stage_cap)) return r;
-    if (int r = alloc_zero(&wk.stage_val, h->esz * stage_cap)) return r;
+    if (int r = alloc_zero(&wk.stage, 2 * h->esz * stage_cap)) return r;
     if (int r = alloc_zero((void**)&wk.chunk_count, 4 * (size_t)(h->tiles + 1) * kChunksPerTile)) return r;
     if (int r = alloc_zero((void**)&wk.tile_count, 4 * (size_t)(h->tiles + 8))) return r;
     if (int r = alloc_zero((void**)&wk.cta_norm, 8 * (size_t)kMaxCtas)) return r;
@@ -381,7 +379,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
       contribs[i] = h->w[i].contrib;
     }
     CU(cudaMalloc((void**)&h->d_lists, sizeof(void*) * n));
-    CU(cudaMemcpy(h->d_p2p_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_lists, lists.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
     CU(cudaMalloc((void**)&h->d_contribs, sizeof(void*) * n));
     CU(cudaMemcpy(h->d_contribs, contribs.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
   }
@@ -419,8 +417,7 @@ void teardown(exd_engine* h) {
     cudaFree(wk.idx);
     cudaFree(wk.val);
     cudaFree(wk.blk);
-    cudaFree(wk.stage_idx);
-    cudaFree(wk.stage_val);
+    cudaFree(wk.stage);
     cudaFree(wk.chunk_count);
     cudaFree(wk.tile_count);
     cudaFree(wk.cta_norm);
@@ -587,8 +584,7 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.idx = wk.idx;
   a.val = wk.val;
   a.blk_counts = wk.blk + (h->t & 1) * h->cfg.n_b;
-  a.stage_idx = wk.stage_idx;
-  a.stage_val = wk.stage_val;
+  a.stage = wk.stage;
   a.chunk_count = wk.chunk_count;
   a.tile_count = wk.tile_count;
   a.tile_norm = wk.tile_norm;

@@ -67,8 +67,7 @@ struct SelectArgs {
   int32_t* idx;             // [cap]    own selection, ascending
   void* val;                // T[cap]   own selected values
   int32_t* blk_counts;      // [n_b]    per-block selection counts
-  int32_t* stage_idx;       // [cap + 2 tiles] warp-chunk staging of the compaction
-  void* stage_val;          // T[...]
+  void* stage;              // [cap + 2 tiles] (index, value) pairs: warp-chunk staging runs
   int32_t* chunk_count;     // [tiles * kChunksPerTile] selected per warp chunk
   int32_t* tile_count;      // [tiles + 4] selected per tile (<= tile size)
   double* tile_norm;        // [tiles] ||e_entering||^2 partial per tile

@@ -280,6 +280,24 @@ __device__ __forceinline__ void control_epilogue_cta(Ctrl* cg, const CountRec* c
 // a pure stream: it runs at the measured copy bandwidth.
 template <typename T> __host__ __device__ constexpr int chunk_of() { return 32 * Vec<T>::N * kUnroll; }
 
+// staged (index, value) pairs: one 8 B (fp32) / 16 B (fp64) store per selected
+// element instead of two scattered ones
+template <typename T> struct Pair;
+template <> struct Pair<float> {
+  using P = uint2;
+  __device__ static P make(uint32_t j, float v) { return make_uint2(j, __float_as_uint(v)); }
+  __device__ static uint32_t idx(const P& p) { return p.x; }
+  __device__ static float val(const P& p) { return __uint_as_float(p.y); }
+};
+template <> struct Pair<double> {
+  using P = ulonglong2;
+  __device__ static P make(uint32_t j, double v) {
+    return make_ulonglong2((unsigned long long)j, (unsigned long long)__double_as_longlong(v));
+  }
+  __device__ static uint32_t idx(const P& p) { return (uint32_t)p.x; }
+  __device__ static double val(const P& p) { return __longlong_as_double((long long)p.y); }
+};
+
 template <typename V>
 __device__ __forceinline__ V warp_sum(V v) {
 #pragma unroll
@@ -357,14 +375,20 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
         sq = fma(ev[u][c], ev[u][c], sq);
         v[u][c] = accumulate<T>(ev[u][c], gv[u][c], rc.eta, UNIT);
       }
+#ifndef EXD_XP_NO_NORM
       nrm += (double)sq;
+#endif
     } else {
 #pragma unroll
       for (int c = 0; c < VN; ++c) v[u][c] = ev[u][c];
     }
   }
 
+#ifdef EXD_XP_NO_SELECT
+  const bool sel_chunk = false;
+#else
   const bool sel_chunk = SELECT && cbeg < end && cbeg + CH > st;
+#endif
   uint32_t flags = 0;
   if (sel_chunk) {
     const T thr = thr_key<T>(ctrl);
@@ -421,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     const uint32_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
     const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
     const bool split = b_lo != b_hi;
-    T* sv = static_cast<T*>(a.stage_val);
+    typename Pair<T>::P* sp = static_cast<typename Pair<T>::P*>(a.stage);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t nib = (flags >> (u * VN)) & ((1u << VN) - 1u);
@@ -435,11 +459,10 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
             const uint32_t j = lbeg + u * 32 * VN + c;
-            a.stage_idx[pos] = (int32_t)j;
-            sv[pos] = v[u][c];
-            // n == 1: the finish kernel will read-modify-write x[j]; pull the
-            // line into L2 now, off everyone's critical path
+            sp[pos] = Pair<T>::make(j, v[u][c]);
+#ifdef EXD_XP_X_PREFETCH
             if (rc.n == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<T*>(a.x) + j));
+#endif
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
             ++pos;
           }
@@ -450,6 +473,9 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
   }
   if (SELECT && lane == 0) a.chunk_count[tile * kWarps + warp] = running;
+#ifdef EXD_XP_NO_TILE
+  return;
+#endif
 
   if (ACCUM) nrm = warp_sum(nrm);
   if (lane == 0) {
@@ -612,8 +638,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   T* __restrict__ val = static_cast<T*>(a.val);
   T* __restrict__ x = static_cast<T*>(a.x);
   int32_t* __restrict__ idx = a.idx;
-  const int32_t* __restrict__ sidx = a.stage_idx;
-  const T* __restrict__ sv = static_cast<const T*>(a.stage_val);
+  const typename Pair<T>::P* __restrict__ sp = static_cast<const typename Pair<T>::P*>(a.stage);
   int64_t running = base;
   for (int cb = 0; cb < nch; cb += kThreads) {
     const int nb = nch - cb < kThreads ? nch - cb : kThreads;
@@ -652,8 +677,9 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
             if (s_off[mid] <= i) lo = mid; else hi = mid;
           }
           const int64_t src = (cbase + lo) * CH + (i - s_off[lo]);
-          jj[q] = __ldcg(&sidx[src]);
-          vv[q] = __ldcg(&sv[src]);
+          const typename Pair<T>::P pr = __ldcg(&sp[src]);
+          jj[q] = (int32_t)Pair<T>::idx(pr);
+          vv[q] = Pair<T>::val(pr);
         }
       }
       if (FUSED) {

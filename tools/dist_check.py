@@ -97,7 +97,8 @@ def main():
                 # the peer-memory sync sums in rank order like the reference
                 same = np.array_equal(m["x"], ox)
             else:
-                same = np.allclose(m["x"], ox, rtol=1e-6, atol=1e-7)
+                # NCCL's reduction order differs from rank order: norm-wise 1e-6
+                same = np.max(np.abs(m["x"] - ox)) <= 1e-6 * max(np.max(np.abs(ox)), 1e-30)
             if not same:
                 print(f"[rank0] rank {r} x differs (max {np.max(np.abs(m['x'] - ox))})", flush=True)
                 ok = False
