@@ -275,6 +275,26 @@ int exd_engine_kernel_stats(exd_engine* h, exd_kernel_stats* out);
 int exd_engine_set_profile(exd_engine* h, int32_t on);
 int exd_engine_reset_kernel_stats(exd_engine* h);
 
+/* ---- ledger ------------------------------------- */
+/* RunStats, runner.hpp:27-40 */
+typedef struct exd_run_stats {
+  int64_t iterations;
+  double mean_density, mean_f, mean_eps;
+  int64_t duplicates;
+  int64_t adjust_moves, adjust_skips, cap_hits;
+  double mean_idle_workers;
+  double final_delta, final_global_err;
+  int32_t has_final_loss;
+  int32_t reserved0;
+  double final_loss;
+} exd_run_stats;
+
+/* format_csv, runner.cpp:55-80: the same bytes (shortest round-trip doubles).
+ * Writes at most cap bytes (NUL-terminated when room); *len gets the full length. */
+int exd_format_csv(const exd_record* recs, int64_t count, char* out, size_t cap, size_t* len);
+/* summarize, runner.cpp:89-113 */
+int exd_summarize(const exd_record* recs, int64_t count, exd_run_stats* out);
+
 /* Writes a buffer larger than L2 on worker w's device (timing hygiene). */
 int exd_flush_l2(int32_t device, void* cuda_stream);
 

@@ -119,8 +119,36 @@ def ref():
         L.ref_engine_last_selection.argtypes = [P, C.c_int32, PI64]
         L.ref_engine_last_union.restype = C.c_int64
         L.ref_engine_last_union.argtypes = [P, PI64]
+        L.ref_format_csv.restype = C.c_int64
+        L.ref_format_csv.argtypes = [C.POINTER(A.exd_record), C.c_int64, C.c_char_p, C.c_int64]
+        L.ref_summarize.argtypes = [C.POINTER(A.exd_record), C.c_int64, PD, PI64]
         _ref = L
     return _ref
+
+
+def records_array(recs):
+    """list of exd_record (or record dicts) -> ctypes array"""
+    arr = (A.exd_record * max(1, len(recs)))()
+    for i, r in enumerate(recs):
+        if isinstance(r, A.exd_record):
+            arr[i] = r
+            continue
+        c = arr[i]
+        for f in A.RECORD_FIELDS:
+            setattr(c, f, r[f])
+        c.has_loss, c.loss = (1, r["loss"]) if r.get("loss") is not None else (0, 0.0)
+        c.n = len(r["k_rank"])
+        for j, k in enumerate(r["k_rank"]):
+            c.k_rank[j] = k
+    return arr
+
+
+def ref_format_csv(recs):
+    arr = records_array(recs)
+    n = ref().ref_format_csv(arr, len(recs), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    ref().ref_format_csv(arr, len(recs), buf, n + 1)
+    return buf.value.decode()
 
 
 class CheckError(Exception):

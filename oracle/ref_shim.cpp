@@ -25,6 +25,7 @@
 #include "sparsim/config.hpp"
 #include "sparsim/engine.hpp"
 #include "sparsim/partition.hpp"
+#include "sparsim/runner.hpp"
 #include "sparsim/selector.hpp"
 #include "sparsim/threshold.hpp"
 #include "sparsim/workloads.hpp"
@@ -387,6 +388,59 @@ int64_t ref_engine_last_union(void* p, int64_t* out) {
   auto* h = static_cast<RefEngine*>(p);
   if (out) std::copy(h->last_union.begin(), h->last_union.end(), out);
   return static_cast<int64_t>(h->last_union.size());
+}
+
+// format_csv / summarize over records given in the C ABI layout
+static IterationRecord to_rec(const exd_record& o) {
+  IterationRecord r;
+  r.t = o.t;
+  r.k_prime = o.k_prime;
+  r.density = o.density;
+  r.eps = o.eps;
+  r.m_t = o.m_t;
+  r.c_t = o.c_t;
+  r.f_t = o.f_t;
+  r.global_err = o.global_err;
+  r.delta = o.delta;
+  if (o.has_loss) r.loss = o.loss;
+  r.duplicates = o.duplicates;
+  r.union_count = o.union_count;
+  r.k_rank.assign(o.k_rank, o.k_rank + o.n);
+  r.adjust_moves = o.adjust_moves;
+  r.adjust_skips = o.adjust_skips;
+  r.cap_hits = o.cap_hits;
+  r.idle_workers = o.idle_workers;
+  return r;
+}
+
+int64_t ref_format_csv(const exd_record* recs, int64_t count, char* out, int64_t cap) {
+  std::vector<IterationRecord> v;
+  for (int64_t i = 0; i < count; ++i) v.push_back(to_rec(recs[i]));
+  const std::string s = format_csv(v);
+  if (out && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, (int64_t)s.size());
+    std::memcpy(out, s.data(), (size_t)n);
+    out[n] = 0;
+  }
+  return (int64_t)s.size();
+}
+
+int ref_summarize(const exd_record* recs, int64_t count, double* out6, int64_t* out5) {
+  std::vector<IterationRecord> v;
+  for (int64_t i = 0; i < count; ++i) v.push_back(to_rec(recs[i]));
+  const RunStats s = summarize(v);
+  out6[0] = s.mean_density;
+  out6[1] = s.mean_f;
+  out6[2] = s.mean_eps;
+  out6[3] = s.mean_idle_workers;
+  out6[4] = s.final_delta;
+  out6[5] = s.final_global_err;
+  out5[0] = s.iterations;
+  out5[1] = s.duplicates;
+  out5[2] = s.adjust_moves;
+  out5[3] = s.adjust_skips;
+  out5[4] = s.cap_hits;
+  return 0;
 }
 
 }  // extern "C"

@@ -89,6 +89,14 @@ class exd_kernel_stats(C.Structure):
                 ("kernel_launches", i64), ("finish_launches", i64), ("finish_ms", f64)]
 
 
+class exd_run_stats(C.Structure):
+    _fields_ = [("iterations", i64), ("mean_density", f64), ("mean_f", f64), ("mean_eps", f64),
+                ("duplicates", i64), ("adjust_moves", i64), ("adjust_skips", i64),
+                ("cap_hits", i64), ("mean_idle_workers", f64), ("final_delta", f64),
+                ("final_global_err", f64), ("has_final_loss", i32), ("reserved0", i32),
+                ("final_loss", f64)]
+
+
 RECORD_FIELDS = ("t", "k_prime", "density", "eps", "m_t", "c_t", "f_t", "global_err",
                  "delta", "duplicates", "union_count", "adjust_moves", "adjust_skips",
                  "cap_hits", "idle_workers")

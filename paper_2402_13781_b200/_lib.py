@@ -92,6 +92,10 @@ def lib():
     _sig(L, "exd_engine_reset_kernel_stats", C.c_int, [P])
     _sig(L, "exd_engine_set_profile", C.c_int, [P, C.c_int32])
     _sig(L, "exd_flush_l2", C.c_int, [C.c_int32, P])
+    _sig(L, "exd_format_csv", C.c_int, [C.POINTER(A.exd_record), C.c_int64, C.c_char_p,
+                                        C.c_size_t, C.POINTER(C.c_size_t)])
+    _sig(L, "exd_summarize", C.c_int, [C.POINTER(A.exd_record), C.c_int64,
+                                       C.POINTER(A.exd_run_stats)])
     _lib = L
     return L
 
@@ -122,5 +126,5 @@ EXPORTED = [
     "exd_engine_step_host", "exd_engine_get_state", "exd_engine_copy_out", "exd_engine_copy_in",
     "exd_engine_device_vector",
     "exd_engine_kernel_stats", "exd_engine_reset_kernel_stats", "exd_engine_set_profile",
-    "exd_flush_l2",
+    "exd_flush_l2", "exd_format_csv", "exd_summarize",
 ]

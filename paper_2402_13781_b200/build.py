@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libexdyna.so")
-SOURCES = ["kernels.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "engine.cu", "ledger.cpp"]
 HEADERS = ["control.cuh", "internal.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -46,7 +46,7 @@ def build(force=False, verbose=False, defines=(), out=None):
     objs = []
     tag = "" if not defines else "_" + "_".join(d.lstrip("-D").lower() for d in defines)
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.replace(".cu", tag + ".o"))
+        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + tag + ".o")
         cmd = [NVCC] + FLAGS + list(defines) + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

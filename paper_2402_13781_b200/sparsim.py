@@ -31,7 +31,8 @@ __all__ = [
     "adjust_topology", "Allocation", "allocate_partition", "scale_threshold",
     "initial_threshold_device", "GatherStats", "gather_stats", "EngineOptions",
     "IterationRecord", "Engine", "StreamSpec", "SyntheticStream", "InvalidArgument",
-    "EngineError", "DeviceError", "Unsupported", "nccl_unique_id", "flush_l2",
+    "EngineError", "DeviceError", "Unsupported", "nccl_unique_id", "flush_l2", "format_csv",
+    "summarize",
 ]
 
 
@@ -261,6 +262,39 @@ class IterationRecord:
     @staticmethod
     def from_c(r):
         return IterationRecord(**A.record_dict(r))
+
+
+def _records_c(records):
+    arr = (A.exd_record * max(1, len(records)))()
+    for i, r in enumerate(records):
+        c = arr[i]
+        for f in A.RECORD_FIELDS:
+            setattr(c, f, getattr(r, f))
+        c.has_loss, c.loss = (1, r.loss) if r.loss is not None else (0, 0.0)
+        c.n = len(r.k_rank)
+        for j, k in enumerate(r.k_rank):
+            c.k_rank[j] = k
+    return arr
+
+
+def format_csv(records) -> str:
+    """runner.cpp:55-80 (same bytes as the reference's CSV ledger)."""
+    arr = _records_c(records)
+    n = C.c_size_t()
+    check(lib().exd_format_csv(arr, len(records), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().exd_format_csv(arr, len(records), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def summarize(records) -> dict:
+    """runner.cpp:89-113 (RunStats)."""
+    s = A.exd_run_stats()
+    check(lib().exd_summarize(_records_c(records), len(records), C.byref(s)))
+    out = {f: getattr(s, f) for f, _ in A.exd_run_stats._fields_ if not f.startswith("reserved")}
+    out["final_loss"] = s.final_loss if s.has_final_loss else None
+    del out["has_final_loss"]
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -260,6 +260,8 @@ def main():
                      "x_sha256": [hashlib.sha256(eng.x(r).tobytes()).hexdigest() for r in range(c.n)],
                      "e_sha256": [hashlib.sha256(eng.e(r).tobytes()).hexdigest() for r in range(c.n)]})
     out["trajectories"] = traj
+    # the reference's CSV ledger (runner.cpp:55-80) of the first trajectory
+    out["csv"] = {"trajectory": 0, "text": O.ref_format_csv([r["record"] for r in traj[0]["rows"]])}
 
     with open(os.path.join(HERE, "reference_golden.json"), "w") as f:
         json.dump(out, f, separators=(",", ":"))

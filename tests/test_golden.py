@@ -213,3 +213,35 @@ def test_oracle_f64_reproduces_reference_trajectories(ti):
     for r in range(cfg.n):
         assert hashlib.sha256(eng.x(r).tobytes()).hexdigest() == tr["x_sha256"][r]
         assert hashlib.sha256(eng.e(r).tobytes()).hexdigest() == tr["e_sha256"][r]
+
+
+# ----------------------------------------------------------------- ledger ---
+def test_format_csv_matches_reference_bytes():
+    """runner.cpp:55-80 through the product's exd_format_csv."""
+    tr = GOLD["trajectories"][GOLD["csv"]["trajectory"]]
+    recs = [S.IterationRecord(**r["record"]) for r in tr["rows"]]
+    assert S.format_csv(recs) == GOLD["csv"]["text"]
+    assert S.format_csv([]) == "t,k_prime,density,eps,m_t,C_t,f_t,global_err,delta,loss\n"
+
+
+def test_summarize_matches_reference():
+    tr = GOLD["trajectories"][1]
+    dicts = [r["record"] for r in tr["rows"]]
+    s = S.summarize([S.IterationRecord(**d) for d in dicts])
+    n = len(dicts)
+    assert s["iterations"] == n
+    acc = 0.0  # sequential, like runner.cpp:94 (Python's sum() is compensated)
+    for d in dicts:
+        acc += d["density"]
+    assert s["mean_density"] == acc / n
+    assert s["final_delta"] == dicts[-1]["delta"]
+    assert s["adjust_moves"] == sum(d["adjust_moves"] for d in dicts)
+    if O.ref_available():
+        arr = O.records_array(dicts)
+        d6 = (C.c_double * 6)()
+        i5 = (C.c_int64 * 5)()
+        O.ref().ref_summarize(arr, n, d6, i5)
+        assert [s["mean_density"], s["mean_f"], s["mean_eps"], s["mean_idle_workers"],
+                s["final_delta"], s["final_global_err"]] == list(d6)
+        assert [s["iterations"], s["duplicates"], s["adjust_moves"], s["adjust_skips"],
+                s["cap_hits"]] == list(i5)
