@@ -203,6 +203,8 @@ struct exd_engine {
   int tile = 0;
   int64_t cap_part = 0;
   long long t = 0;                    // steps enqueued
+  int64_t cap = 0;                    // per-rank density cap (0: none)
+  bool union_flow = false;            // union / reduce / finalize kernels run (n > 1 or cap)
   // shared device buffers
   CountRec* counts_all = nullptr;     // [n]
   CountRec* counts_host = nullptr;    // pinned (dist)
@@ -274,12 +276,16 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   if (cfg.n_g > 0x7fffffffLL) return set_err(EXD_EINVAL, "gradient count exceeds int32 index range");
   if (opt->sparsifier != EXD_SPARSIFIER_EXDYNA)
     return set_err(EXD_EUNSUPPORTED, "only the ExDyna sparsifier is on the B200 path");
-  if (cfg.has_max_density_cap)
-    return set_err(EXD_EUNSUPPORTED, "max_density_cap is not implemented on the B200 path");
   if (opt->dtype != EXD_F32 && opt->dtype != EXD_F64) return set_err(EXD_EINVAL, "dtype out of range");
   h->cfg = cfg;
   h->opt = *opt;
   h->n = cfg.n;
+  // engine.cpp:166-171: cap = max(1, llround(max_density_cap * n_g / n))
+  if (cfg.has_max_density_cap) {
+    const int64_t c = (int64_t)std::llround(cfg.max_density_cap * (double)cfg.n_g / cfg.n);
+    h->cap = c > 1 ? c : 1;
+  }
+  h->union_flow = cfg.n > 1 || h->cap > 0;
   h->esz = elem_size(opt->dtype);
   h->tiles = num_tiles(cfg.n_g, opt->dtype);
   h->tile = tile_elems(opt->dtype);
@@ -299,7 +305,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   h->w.resize(n_local);
   if (int rc = alloc_zero((void**)&h->counts_all, sizeof(CountRec) * n)) return rc;
   CU(cudaHostAlloc((void**)&h->counts_host, sizeof(CountRec) * n, cudaHostAllocDefault));
-  if (n > 1) {
+  if (h->union_flow) {
     if (int rc = alloc_zero(&h->sum, h->esz * ng)) return rc;
   }
   if (int rc = alloc_zero(&h->qscratch, quantile_scratch_bytes())) return rc;
@@ -326,6 +332,8 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     rc.min_blk = cfg.min_blk;
     rc.static_partitions = opt->static_partitions;
     rc.dtype = opt->dtype;
+    rc.cap = h->cap;
+    rc.fused = (n == 1 && h->cap == 0) ? 1 : 0;
     blk_magic(topo0.sz_blk, &rc.blk_magic, &rc.blk_shift);
     if (int r = alloc_zero(&wk.x, h->esz * ng)) return r;
     if (int r = alloc_zero(&wk.e, h->esz * ng)) return r;
@@ -339,14 +347,14 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero((void**)&wk.cta_norm, 8 * (size_t)kMaxCtas)) return r;
     if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
     if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
-    if (n > 1) {
+    if (h->union_flow) {
       if (int r = alloc_zero((void**)&wk.idx_global, 4 * ng)) return r;
       if (int r = alloc_zero(&wk.contrib, h->esz * ng)) return r;
     }
-    if (h->dist) {
-      if (int r = alloc_zero((void**)&wk.cnt, sizeof(CountRec))) return r;
+    if (h->dist && n > 1) {
+      if (int r = alloc_zero((void**)&wk.cnt, sizeof(CountRec))) return r;  // all-gather source
     } else {
-      wk.cnt = h->counts_all + wk.rank;
+      wk.cnt = h->counts_all + (h->dist ? 0 : wk.rank);
     }
     CU(cudaHostAlloc((void**)&wk.rec_host, sizeof(exd_record), cudaHostAllocDefault));
     std::memset(wk.rec_host, 0, sizeof(exd_record));
@@ -371,7 +379,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   }
   CU(cudaMalloc((void**)&h->d_ctrls, sizeof(Ctrl*) * n_local));
   CU(cudaMemcpy(h->d_ctrls, ctrls.data(), sizeof(Ctrl*) * n_local, cudaMemcpyHostToDevice));
-  if (!h->dist && n > 1) {
+  if (!(h->dist && n > 1) && h->union_flow) {
     std::vector<const int32_t*> lists(n);
     std::vector<const void*> contribs(n);
     for (int i = 0; i < n; ++i) {
@@ -426,7 +434,7 @@ void teardown(exd_engine* h) {
     cudaFree(wk.idx_global);
     cudaFree(wk.contrib);
     cudaFree(wk.grad_stage);
-    if (h->dist) cudaFree(wk.cnt);
+    if (h->dist && h->n > 1) cudaFree(wk.cnt);
     cudaFreeHost(wk.rec_host);
     cudaFree(wk.rec_dev);
   }
@@ -595,8 +603,9 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.tile_base = 0;
   a.num_tiles = (int32_t)h->tiles;
   a.t = h->t;
-  a.push_idx = h->p2p ? h->d_push : nullptr;
-  a.npush = h->p2p ? h->n - 1 : 0;
+  // with a cap the list is pushed only after it is trimmed (cap kernel)
+  a.push_idx = (h->p2p && h->cap == 0) ? h->d_push : nullptr;
+  a.npush = (h->p2p && h->cap == 0) ? h->n - 1 : 0;
   return a;
 }
 
@@ -647,8 +656,26 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
     }
   }
 
-  if (n > 1) {
-    if (h->dist && h->p2p) {
+  // density cap on each worker's compacted selection (selector.cpp:44-61)
+  if (h->cap > 0) {
+    for (int i = 0; i < nl; ++i) {
+      Worker& wk = h->w[i];
+      CapArgs ca{};
+      ca.idx = wk.idx;
+      ca.val = wk.val;
+      ca.e = wk.e;
+      ca.blk_counts = wk.blk + (h->t & 1) * c.n_b;
+      ca.cnt = wk.cnt;
+      ca.ctrl = wk.ctrl;
+      ca.push = h->p2p ? h->d_push : nullptr;
+      ca.npush = h->p2p ? n - 1 : 0;
+      CU(launch_cap(ca, wk.rc, h->stream));
+      h->stats.kernel_launches += 1;
+    }
+  }
+
+  if (h->union_flow) {
+    if (h->dist && n > 1 && h->p2p) {
       // f1: peer-memory sync, no host wait, no NCCL
       Worker& wk = h->w[0];
       P2PArgs pa{};
@@ -672,7 +699,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       CU(launch_p2p_union(pa, wk.rc, h->stream));
       CU(launch_p2p_reduce(pa, wk.rc, h->stream));
       h->stats.kernel_launches += 2;
-    } else if (h->dist) {
+    } else if (h->dist && n > 1) {
       Worker& wk = h->w[0];
       NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));
       CU(cudaMemcpyAsync(h->counts_host, h->counts_all, sizeof(CountRec) * n,
@@ -1043,7 +1070,7 @@ int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t
     case EXD_VEC_E: *n_el = h->cfg.n_g; *src = wk.e; break;
     case EXD_VEC_IDX_GLOBAL:
       *n_el = h->has_record ? rec.k_prime : 0;
-      *src = h->n > 1 ? (const void*)wk.idx_global : (const void*)wk.idx;
+      *src = h->union_flow ? (const void*)wk.idx_global : (const void*)wk.idx;
       es = 4;
       break;
     case EXD_VEC_LOCAL_IDX:
@@ -1062,7 +1089,7 @@ int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t
       break;
     case EXD_VEC_SUM:
       *n_el = h->has_record ? rec.k_prime : 0;
-      *src = h->n > 1 ? h->sum : wk.val;
+      *src = h->union_flow ? h->sum : wk.val;
       break;
     default:
       return set_err(EXD_EINVAL, "unknown vector");

@@ -42,10 +42,12 @@ struct Ctrl {
   double norm2;             // ||e_entering||^2 of the running step
 };
 
-// What each rank contributes to the count all-gather (16 bytes).
+// What each rank contributes to the count all-gather (32 bytes).
 struct CountRec {
   int64_t k;
   double norm2;
+  int64_t capped;          // the density cap trimmed this rank's selection
+  int64_t reserved;
 };
 
 // Everything a kernel needs to know about the run (by value).
@@ -58,6 +60,8 @@ struct RunConst {
   int32_t dtype;
   unsigned long long blk_magic;  // j / sz_blk == (j * blk_magic) >> blk_shift for j < 2^31
   int32_t blk_shift;
+  int32_t fused;                 // n == 1 without a cap: x update + epilogue in the finish kernel
+  int64_t cap;                   // per-rank density cap (engine.cpp:166-171); 0 = none
 };
 
 struct SelectArgs {
@@ -116,7 +120,8 @@ struct PeerFlags {                   // inbox[src] on the receiver
   int64_t k;
   double norm2;
   unsigned long long contrib_epoch;  // src's contributions of step epoch-1 are readable
-  unsigned long long pad[12];        // 128 B: one slot per line
+  int64_t capped;
+  unsigned long long pad[11];        // 128 B: one slot per line
 };
 
 struct P2PArgs {
@@ -157,6 +162,18 @@ cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void
                                       const void* xw, int64_t n_g, int dtype, int32_t w,
                                       uint32_t* flag, cudaStream_t s);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
+// density cap (selector.cpp:44-61) on the compacted own selection
+struct CapArgs {
+  int32_t* idx;                  // [k_i] own selection, ascending (compacted in place)
+  void* val;                     // [k_i] own values (T)
+  void* e;                       // residual: dropped elements get their acc back
+  int32_t* blk_counts;           // per-block counts of this step
+  CountRec* cnt;                 // own {k_i, norm2, capped}
+  Ctrl* ctrl;
+  int32_t* const* push;          // P2P: [npush] my list slot in every peer's inbox
+  int32_t npush;
+};
+cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,

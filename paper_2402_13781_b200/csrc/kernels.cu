@@ -156,8 +156,8 @@ __device__ __noinline__ void make_plan(Plan* p, const exd_topology* base, const 
 }
 
 __device__ __noinline__ void make_record(exd_record* rec, const int64_t* k_rank,
-                                         const double* norm2, int64_t t, double delta_used,
-                                         const Plan* cur, const RunConst& rc) {
+                                         const double* norm2, const int64_t* capped, int64_t t,
+                                         double delta_used, const Plan* cur, const RunConst& rc) {
   const int n = rc.n;
   double norm_sum = 0.0;
   for (int r = 0; r < n; ++r) norm_sum = __dadd_rn(norm_sum, sqrt(norm2[r]));
@@ -181,7 +181,9 @@ __device__ __noinline__ void make_record(exd_record* rec, const int64_t* k_rank,
   rec->n = n;
   rec->adjust_moves = cur->moves;
   rec->adjust_skips = cur->skips;
-  rec->cap_hits = 0;
+  int cap_hits = 0;  // engine.cpp:345
+  for (int r = 0; r < n; ++r) cap_hits += capped[r] ? 1 : 0;
+  rec->cap_hits = cap_hits;
   rec->idle_workers = 0;
   rec->reserved1 = 0;
   for (int r = 0; r < n; ++r) rec->k_rank[r] = k_rank[r];
@@ -213,6 +215,7 @@ struct EpiShared {
   exd_record rec;
   int64_t k_rank[EXD_MAX_WORKERS];
   double norm2[EXD_MAX_WORKERS];
+  int64_t capped[EXD_MAX_WORKERS];
 };
 
 __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
@@ -238,7 +241,7 @@ __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const Run
   } else if (tid == 32) {
     make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, t + 1, rc);
   } else if (tid == 64 && rec_out) {
-    make_record(&sh.rec, sh.k_rank, sh.norm2, t, delta_used, &sh.c.plan[t & 1], rc);
+    make_record(&sh.rec, sh.k_rank, sh.norm2, sh.capped, t, delta_used, &sh.c.plan[t & 1], rc);
   }
   __syncthreads();
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
@@ -260,6 +263,7 @@ __device__ __forceinline__ void control_epilogue_cta(Ctrl* cg, const CountRec* c
   for (int r = threadIdx.x; r < rc.n; r += blockDim.x) {
     sh.k_rank[r] = __ldcg(&counts[r].k);
     sh.norm2[r] = __ldcg(&counts[r].norm2);
+    sh.capped[r] = __ldcg(&counts[r].capped);
   }
   __syncthreads();
   PROBE(4);
@@ -602,11 +606,13 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
       }
       a.cnt_out->k = kt;
       a.cnt_out->norm2 = n2;
+      a.cnt_out->capped = 0;
       if (FUSED) {
         esh.c.k_local = kt;
         esh.c.norm2 = n2;
         esh.k_rank[0] = kt;
         esh.norm2[0] = n2;
+        esh.capped[0] = 0;
       } else {
         ctrl->k_local = kt;
         ctrl->norm2 = n2;
@@ -749,7 +755,7 @@ cudaError_t launch_finish_t(const SelectArgs& a, const RunConst& rc, cudaStream_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (rc.n == 1) return cudaLaunchKernelEx(&cfg, finish_kernel<T, true>, a, rc);
+  if (rc.fused) return cudaLaunchKernelEx(&cfg, finish_kernel<T, true>, a, rc);
   return cudaLaunchKernelEx(&cfg, finish_kernel<T, false>, a, rc);
 }
 
@@ -939,6 +945,7 @@ __global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) 
     PeerFlags* slot = a.peer_slot[tid];
     st_relaxed_sys_i64(&slot->k, a.own_cnt->k);
     st_relaxed_sys_f64(&slot->norm2, a.own_cnt->norm2);
+    st_relaxed_sys_i64(&slot->capped, a.own_cnt->capped);
     asm volatile("fence.acq_rel.sys;" ::: "memory");
     st_relaxed_sys(&slot->count_epoch, a.epoch);
   }
@@ -960,6 +967,7 @@ __global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) 
   if (blockIdx.x == 0 && tid < n) {
     a.counts_all[tid].k = __ldcg(&a.inbox[tid].k);
     a.counts_all[tid].norm2 = __ldcg(&a.inbox[tid].norm2);
+    a.counts_all[tid].capped = __ldcg(&a.inbox[tid].capped);
   }
   __syncthreads();
   const int64_t kp = s_off[n];
@@ -1060,6 +1068,155 @@ __global__ void __launch_bounds__(256) p2p_reduce_kernel(P2PArgs a, RunConst rc)
   if (blockIdx.x == 0) PROBE(25);
 }
 
+template <typename T> struct Bits;
+template <> struct Bits<float> {
+  using U = uint32_t;
+  static constexpr int W = 32;
+  __device__ static U abs_bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+};
+template <> struct Bits<double> {
+  using U = unsigned long long;
+  static constexpr int W = 64;
+  __device__ static U abs_bits(double v) {
+    return (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+  }
+};
+
+// ---- density cap (selector.cpp:44-61, engine.cpp:164-186) --------------------
+// When a rank selected more than cap = max(1, llround(cap_frac * n_g / n))
+// elements, keep the cap largest |acc| (ties: lower index first), in ascending
+// index order. One CTA works on the compacted list (k_i entries): an 8-bit
+// radix select finds V, the (k_i - cap)-th smallest |acc| (nth_element's
+// partition point); everything above V is kept, and of the elements equal to V
+// the first (cap - #above) in index order. Dropped elements get their residual
+// back (they are not in the union) and leave the per-block counts.
+constexpr int kCapThreads = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kCapThreads) cap_kernel(CapArgs a, RunConst rc) {
+  using U = typename Bits<T>::U;
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ long long s_rank;
+  __shared__ int s_wsum[kCapThreads / 32];
+  __shared__ int s_wsum2[kCapThreads / 32];
+  __shared__ long long s_gt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ki = a.cnt->k;
+  const int64_t cap = rc.cap;
+  T* val = static_cast<T*>(a.val);
+  T* e = static_cast<T*>(a.e);
+  if (ki <= cap) {
+    if (tid == 0) a.cnt->capped = 0;
+    for (int64_t i = tid; i < ki; i += kCapThreads)
+      for (int p = 0; p < a.npush; ++p) a.push[p][i] = a.idx[i];
+    return;
+  }
+  // radix select of the pos-th smallest |val|, pos = k_i - cap
+  if (tid == 0) {
+    s_prefix = 0;
+    s_mask = 0;
+    s_rank = ki - cap;
+  }
+  for (int shift = Bits<T>::W - 8; shift >= 0; shift -= 8) {
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix, mask = s_mask;
+    for (int64_t i = tid; i < ki; i += kCapThreads) {
+      const unsigned long long b = Bits<T>::abs_bits(val[i]);
+      if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 0xffu], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long r = s_rank;
+      int d = 0;
+      for (; d < 256; ++d) {
+        if (r < (long long)hist[d]) break;
+        r -= hist[d];
+      }
+      s_rank = r;
+      s_prefix |= (unsigned long long)d << shift;
+      s_mask |= 0xffULL << shift;
+    }
+    __syncthreads();
+  }
+  const unsigned long long V = s_prefix;
+  // #elements strictly above V
+  int gt = 0;
+  for (int64_t i = tid; i < ki; i += kCapThreads) gt += Bits<T>::abs_bits(val[i]) > V;
+  gt = warp_sum(gt);
+  if (lane == 0) s_wsum[warp] = gt;
+  __syncthreads();
+  if (tid == 0) {
+    long long sgt = 0;
+    for (int w = 0; w < kCapThreads / 32; ++w) sgt += s_wsum[w];
+    s_gt = sgt;
+  }
+  __syncthreads();
+  const long long keep_ties = cap - s_gt;
+  // order-preserving in-place compaction, one chunk of kCapThreads at a time
+  long long ties_before = 0, out = 0;
+  for (int64_t base = 0; base < ki; base += kCapThreads) {
+    const int64_t i = base + tid;
+    int32_t j = 0;
+    T v = T(0);
+    int is_tie = 0, above = 0;
+    if (i < ki) {
+      j = a.idx[i];
+      v = val[i];
+      const unsigned long long b = Bits<T>::abs_bits(v);
+      above = b > V;
+      is_tie = b == V;
+    }
+    // exclusive scan of is_tie over the chunk (tie rank), then of keep
+    int tincl = is_tie;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, tincl, o);
+      if (lane >= o) tincl += y;
+    }
+    if (lane == 31) s_wsum[warp] = tincl;
+    __syncthreads();
+    int wpre = 0, ttot = 0;
+    for (int w = 0; w < kCapThreads / 32; ++w) {
+      wpre += w < warp ? s_wsum[w] : 0;
+      ttot += s_wsum[w];
+    }
+    const long long tie_rank = ties_before + wpre + tincl - is_tie;
+    const int keep = (i < ki) && (above || (is_tie && tie_rank < keep_ties));
+    int kincl = keep;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, kincl, o);
+      if (lane >= o) kincl += y;
+    }
+    if (lane == 31) s_wsum2[warp] = kincl;
+    __syncthreads();  // every read of this chunk is done before anyone writes
+    int kpre = 0, ktot = 0;
+    for (int w = 0; w < kCapThreads / 32; ++w) {
+      kpre += w < warp ? s_wsum2[w] : 0;
+      ktot += s_wsum2[w];
+    }
+    if (keep) {
+      const int64_t o = out + kpre + kincl - 1;
+      a.idx[o] = j;
+      val[o] = v;
+      for (int p = 0; p < a.npush; ++p) a.push[p][o] = j;
+    } else if (i < ki) {
+      e[j] = v;  // not in the union: the residual keeps acc (selector.cpp:63-65)
+      atomicAdd(&a.blk_counts[block_of((uint32_t)j, rc)], -1);
+    }
+    ties_before += ttot;
+    out += ktot;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.cnt->k = cap;
+    a.cnt->capped = 1;
+    a.ctrl->k_local = cap;
+  }
+}
+
 // ---- delta0 broadcast into every worker's control block ---------------------
 template <typename T>
 __global__ void set_delta_kernel(Ctrl* const* ctrls, int nctrl, const void* bits) {
@@ -1080,20 +1237,6 @@ struct QState {
   unsigned long long prefix, mask;
   long long rank;
   unsigned int hist[256];
-};
-
-template <typename T> struct Bits;
-template <> struct Bits<float> {
-  using U = uint32_t;
-  static constexpr int W = 32;
-  __device__ static U abs_bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
-};
-template <> struct Bits<double> {
-  using U = unsigned long long;
-  static constexpr int W = 64;
-  __device__ static U abs_bits(double v) {
-    return (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
-  }
 };
 
 template <typename T>
@@ -1347,6 +1490,12 @@ cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s) {
   const int blocks = p2p_blocks() + 1;
   if (rc.dtype == EXD_F64) return launch_pdl(p2p_reduce_kernel<double>, blocks, s, a, rc);
   return launch_pdl(p2p_reduce_kernel<float>, blocks, s, a, rc);
+}
+
+cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {
+  if (rc.dtype == EXD_F64) cap_kernel<double><<<1, kCapThreads, 0, s>>>(a, rc);
+  else cap_kernel<float><<<1, kCapThreads, 0, s>>>(a, rc);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_set_delta(Ctrl* const* ctrls, int nctrl, const void* bits, int dtype,

@@ -61,11 +61,14 @@ class Pair:
         self.torch.cuda.synchronize()
         return [b.cpu().numpy() for b in self.bufs]
 
-    def step(self, t, scale=None):
+    def step(self, t, scale=None, quantum=None):
         host = self.gradients(t)
-        if scale is not None:
+        if scale is not None or quantum is not None:
             for b in self.bufs:
-                b.mul_(scale)
+                if scale is not None:
+                    b.mul_(scale)
+                if quantum is not None:  # coarse grid: many equal magnitudes (ties)
+                    b.copy_(self.torch.round(b / quantum) * quantum)
             self.torch.cuda.synchronize()
             host = [b.cpu().numpy() for b in self.bufs]
         rec = self.eng.step(self.bufs)

@@ -280,8 +280,6 @@ def test_device_quantile_matches_nth_element(dtype):
 def test_kernel_stats_and_unsupported_options():
     import torch
     with pytest.raises(S.Unsupported):
-        S.Engine(S.SparsifierConfig(n=2, n_g=1000, n_b=8, d=0.01, max_density_cap=0.5))
-    with pytest.raises(S.Unsupported):
         S.Engine(S.SparsifierConfig(n=2, n_g=1000, n_b=8, d=0.01), S.EngineOptions(sparsifier="topk"))
     eng = S.Engine(S.SparsifierConfig(n=1, n_g=100_000, n_b=8, d=0.01),
                    S.EngineOptions(profile_kernels=True))
@@ -291,3 +289,36 @@ def test_kernel_stats_and_unsupported_options():
     st = eng.kernel_stats()
     # t=0 without delta0: accumulate + select-only launches, then one fused launch per step
     assert st["select_launches"] == 4 and st["select_ms"] > 0 and st["steps"] == 3
+
+
+CAP_CONFIGS = [
+    dict(n=1, n_g=40_000, n_b=8, d=0.02, seed=3, max_density_cap=0.006),
+    dict(n=2, n_g=100_001, n_b=32, d=0.02, seed=4, max_density_cap=0.005),
+    dict(n=3, n_g=60_000, n_b=24, d=0.05, seed=5, max_density_cap=0.01, beta=1.05),
+]
+
+
+@pytest.mark.parametrize("kw", CAP_CONFIGS, ids=lambda k: f"n{k['n']}")
+@pytest.mark.parametrize("quantum", [None, 0.25])
+def test_density_cap_fp32_vs_oracle(kw, quantum):
+    """selector.cpp:44-61: cap hits, kept set (largest |acc|, lower index on
+    ties), restored residuals and cap_hits in the ledger, bit-exact."""
+    p = Pair(kw, "f32")
+    hits = 0
+    for t in range(15):
+        rec, orec = p.step(t, quantum=quantum)
+        check_record(rec, orec, ctx=f"t={t}")
+        p.compare_selection(ctx=f"t={t}")
+        hits += rec.cap_hits
+    p.compare_state(ctx="end")
+    assert hits > 0
+
+
+@pytest.mark.parametrize("kw", CAP_CONFIGS[:2], ids=lambda k: f"n{k['n']}")
+def test_density_cap_fp64_vs_reference(kw):
+    checker = "reference" if O.ref_available() else "oracle"
+    p = Pair(kw, "f64", checker=checker)
+    for t in range(12):
+        rec, orec = p.step(t)
+        check_record(rec, orec, ctx=f"t={t}")
+    p.compare_state(ctx="end")

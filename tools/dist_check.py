@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--d", type=float, default=0.01)
     ap.add_argument("--skew", type=int, default=1)
     ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p"])
+    ap.add_argument("--cap", type=float, default=None, help="max_density_cap")
     args = ap.parse_args()
 
     import numpy as np
@@ -40,7 +41,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    kw = dict(n=world, n_g=args.n_g, n_b=max(16, 8 * world), d=args.d, seed=5, beta=1.05)
+    kw = dict(n=world, n_g=args.n_g, n_b=max(16, 8 * world), d=args.d, seed=5, beta=1.05,
+              max_density_cap=args.cap)
     ids = [S.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     eng = S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype="f32", sync=args.sync),
@@ -64,7 +66,7 @@ def main():
             orec = orc.step(host)
             o = O.A.record_dict(orec)
             for f in ("k_prime", "m_t", "c_t", "f_t", "delta", "density", "eps", "adjust_moves",
-                      "adjust_skips", "union_count"):
+                      "adjust_skips", "union_count", "cap_hits"):
                 if getattr(rec, f) != o[f]:
                     print(f"[rank0] t={t} {f}: gpu={getattr(rec, f)} oracle={o[f]}", flush=True)
                     ok = False
@@ -105,7 +107,7 @@ def main():
             if not np.array_equal(m["sel"].astype(np.int64), orc.selection(r)):
                 print(f"[rank0] rank {r} selection differs", flush=True)
                 ok = False
-        print(f"dist_check world={world} sync={args.sync} n_g={args.n_g} steps={args.steps}: "
+        print(f"dist_check world={world} sync={args.sync} cap={args.cap} n_g={args.n_g} steps={args.steps}: "
               f"{'PASS' if ok else 'FAIL'} (last k'={rec.k_prime} f_t={rec.f_t:.3f})", flush=True)
     flag = torch.tensor([1 if ok else 0])
     dist.broadcast(flag, src=0)
