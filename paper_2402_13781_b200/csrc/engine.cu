@@ -185,6 +185,8 @@ struct Worker {
   int32_t* idx_global = nullptr;
   void* contrib = nullptr;
   void* grad_stage = nullptr;         // exd_engine_step_host staging
+  void* snapshot = nullptr;           // verify_conservation: acc of the running step
+  uint32_t* bitmap = nullptr;         // verify_conservation: union membership
   exd_record* rec_host = nullptr;     // pinned: last record copied back at sync
   exd_record* rec_dev = nullptr;      // device ring of kRecRing records (slot t % kRecRing)
   Plan plan0{};                       // host copy of the t = 0 plan
@@ -231,6 +233,7 @@ struct exd_engine {
   unsigned int* p2p_err = nullptr;    // pinned host copy
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [2] local gate words
+  void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
   // profiling
@@ -347,6 +350,10 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero((void**)&wk.cta_norm, 8 * (size_t)kMaxCtas)) return r;
     if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
     if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
+    if (opt->verify_conservation) {
+      if (int r = alloc_zero(&wk.snapshot, h->esz * ng)) return r;
+      if (int r = alloc_zero((void**)&wk.bitmap, 4 * ((ng + 31) / 32))) return r;
+    }
     if (h->union_flow) {
       if (int r = alloc_zero((void**)&wk.idx_global, 4 * ng)) return r;
       if (int r = alloc_zero(&wk.contrib, h->esz * ng)) return r;
@@ -434,6 +441,8 @@ void teardown(exd_engine* h) {
     cudaFree(wk.idx_global);
     cudaFree(wk.contrib);
     cudaFree(wk.grad_stage);
+    cudaFree(wk.snapshot);
+    cudaFree(wk.bitmap);
     if (h->dist && h->n > 1) cudaFree(wk.cnt);
     cudaFreeHost(wk.rec_host);
     cudaFree(wk.rec_dev);
@@ -531,6 +540,8 @@ int setup_p2p(exd_engine* h) {
     con[r] = base[r] + off_c0;
     con[n + r] = base[r] + off_c1;
   }
+  h->p2p_own_contrib[0] = own + off_c0;
+  h->p2p_own_contrib[1] = own + off_c1;
   CU(cudaMalloc((void**)&h->d_slot, sizeof(void*) * n));
   CU(cudaMalloc((void**)&h->d_p2p_lists, sizeof(void*) * n));
   CU(cudaMalloc((void**)&h->d_push, sizeof(void*) * (n > 1 ? n - 1 : 1)));
@@ -620,6 +631,14 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   // zero the other parity's block counters for the next step
   for (auto& wk : h->w)
     CU(cudaMemsetAsync(wk.blk + ((h->t + 1) & 1) * c.n_b, 0, 4 * (size_t)c.n_b, h->stream));
+
+  // verify_conservation (engine.cpp:142): acc snapshot of every worker
+  if (h->opt.verify_conservation) {
+    for (int i = 0; i < nl; ++i) {
+      CU(launch_snapshot(h->w[i].e, grads[i], h->w[i].snapshot, h->w[i].rc, h->stream));
+      h->stats.kernel_launches += 1;
+    }
+  }
 
   if (h->t == 0 && !c.has_delta0) {
     // accumulate_phase, then initialize_threshold (engine.cpp:146-161) on
@@ -755,7 +774,6 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
         u.ctrl = wk.ctrl;
         CU(launch_union(u, wk.rc, h->stream));
         h->stats.kernel_launches += 1;
-      h->stats.kernel_launches += 1;
       }
       CU(launch_allreduce_local(h->d_contribs, h->sum, h->w[0].ctrl, h->counts_all, h->w[0].rc,
                                 h->stream));
@@ -771,9 +789,24 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
         f.rec = wk.rec_dev + (h->t % kRecRing);
         CU(launch_finalize(f, wk.rc, h->stream));
         h->stats.kernel_launches += 1;
-      h->stats.kernel_launches += 1;
       }
     }
+  }
+  // verify_conservation, engine.cpp:221-249 (each worker against its snapshot)
+  if (h->opt.verify_conservation) {
+    for (int i = 0; i < nl; ++i) {
+      Worker& wk = h->w[i];
+      const int32_t* uni = h->union_flow ? wk.idx_global : wk.idx;
+      const void* contrib = !h->union_flow ? wk.val
+                            : (h->dist && n > 1 && h->p2p) ? h->p2p_own_contrib[h->t & 1]
+                                                           : wk.contrib;
+      const CountRec* cnts = h->union_flow ? h->counts_all : wk.cnt;
+      const int ncnt = h->union_flow ? n : 1;
+      CU(launch_conservation(uni, cnts, ncnt, contrib, wk.e, wk.snapshot, wk.bitmap,
+                             h->verify_flag_dev, wk.rc, h->stream));
+      h->stats.kernel_launches += 2;
+    }
+    h->verify_t = h->t;
   }
   // verify_replication, engine.cpp:251-272 (in-process replicas)
   if (h->opt.verify_replication && !h->dist && nl > 1) {
@@ -814,10 +847,18 @@ int sync_engine(exd_engine* h, exd_record* out) {
   }
   if (*h->verify_flag) {
     const uint32_t f = *h->verify_flag;
-    const char* field = (f & 1) ? "delta" : (f & 2) ? "k_t" : (f & 4) ? "topology" : "x";
     char msg[160];
-    std::snprintf(msg, sizeof msg, "replicated state diverged at iteration %lld: rank %u field %s",
-                  (long long)h->verify_t, f >> 8, field);
+    if (f >= 0x10000u) {  // engine.cpp:229-245
+      const uint32_t code = f >> 16;
+      const char* what = code == 1 ? "contribution != acc" : code == 2 ? "residual not cleared"
+                                                                      : "unselected residual changed";
+      std::snprintf(msg, sizeof msg, "conservation violated: %s at t=%lld", what,
+                    (long long)h->verify_t);
+    } else {
+      const char* field = (f & 1) ? "delta" : (f & 2) ? "k_t" : (f & 4) ? "topology" : "x";
+      std::snprintf(msg, sizeof msg, "replicated state diverged at iteration %lld: rank %u field %s",
+                    (long long)h->verify_t, (f >> 8) & 0xffu, field);
+    }
     *h->verify_flag = 0;
     return set_err(EXD_EINVARIANT, msg);
   }

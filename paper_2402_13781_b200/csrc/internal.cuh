@@ -174,6 +174,10 @@ struct CapArgs {
   int32_t npush;
 };
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s);
+cudaError_t launch_snapshot(const void* e, const void* g, void* snap, RunConst rc, cudaStream_t s);
+cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int ncounts,
+                                const void* contrib, const void* e, const void* snap,
+                                uint32_t* bitmap, uint32_t* flag, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,

@@ -1331,6 +1331,58 @@ __global__ void verify_kernel(const Ctrl* c0, const Ctrl* cw, const T* x0, const
   if (bits) atomicCAS(flag, 0u, ((uint32_t)w << 8) | bits);
 }
 
+// ---- verify_conservation (engine.cpp:221-249), debug option -----------------
+// snapshot: acc = e + eta*g with the stream kernel's exact arithmetic, taken
+// before the step; after it: every contribution equals the snapshot at its
+// union index, the residual is cleared there, and untouched everywhere else.
+// Violations are reported through `flag` as 0x10000 * code | rank << 8.
+template <typename T>
+__global__ void __launch_bounds__(256) snapshot_kernel(const T* e, const T* g, T* snap, int64_t n_g,
+                                                       double eta) {
+  const bool unit = eta == 1.0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_g;
+       j += (int64_t)gridDim.x * blockDim.x)
+    snap[j] = accumulate<T>(e[j], g[j], eta, unit);
+}
+
+template <typename T> __device__ __forceinline__ bool same_bits(T a, T b);
+template <> __device__ __forceinline__ bool same_bits<float>(float a, float b) {
+  return __float_as_uint(a) == __float_as_uint(b);
+}
+template <> __device__ __forceinline__ bool same_bits<double>(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) conserve_union_kernel(const int32_t* uni, const CountRec* counts,
+                                                             int n, const T* contrib, const T* e,
+                                                             const T* snap, uint32_t* bitmap,
+                                                             uint32_t* flag, uint32_t rank) {
+  int64_t kp = 0;
+  for (int r = 0; r < n; ++r) kp += counts[r].k;
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < kp;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = uni[pos];
+    if (!same_bits<T>(contrib[pos], snap[j])) atomicCAS(flag, 0u, 0x10000u | (rank << 8));
+    if (e[j] != T(0)) atomicCAS(flag, 0u, 0x20000u | (rank << 8));
+    atomicOr(&bitmap[j >> 5], 1u << (j & 31));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) conserve_rest_kernel(const T* e, const T* snap,
+                                                            const uint32_t* bitmap, int64_t n_g,
+                                                            uint32_t* flag, uint32_t rank) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_g;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if ((bitmap[j >> 5] >> (j & 31)) & 1u) continue;
+    if (!same_bits<T>(e[j], snap[j])) {
+      atomicCAS(flag, 0u, 0x30000u | (rank << 8));
+      return;
+    }
+  }
+}
+
 // ---- device GradientSource: workloads.cpp:62-85 + rng.hpp:28-59 ----------
 struct SegTable {
   int32_t nseg;
@@ -1495,6 +1547,44 @@ cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s) {
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {
   if (rc.dtype == EXD_F64) cap_kernel<double><<<1, kCapThreads, 0, s>>>(a, rc);
   else cap_kernel<float><<<1, kCapThreads, 0, s>>>(a, rc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_snapshot(const void* e, const void* g, void* snap, RunConst rc, cudaStream_t s) {
+  const int blocks = grid_for(rc.n_g, 256 * 8);
+  if (rc.dtype == EXD_F64)
+    snapshot_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(e),
+                                                   static_cast<const double*>(g),
+                                                   static_cast<double*>(snap), rc.n_g, rc.eta);
+  else
+    snapshot_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(e),
+                                                  static_cast<const float*>(g),
+                                                  static_cast<float*>(snap), rc.n_g, rc.eta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int ncounts,
+                                const void* contrib, const void* e, const void* snap,
+                                uint32_t* bitmap, uint32_t* flag, RunConst rc, cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(bitmap, 0, 4 * (size_t)((rc.n_g + 31) / 32), s);
+  if (err != cudaSuccess) return err;
+  const int blocks = grid_for(rc.n_g, 256 * 8);
+  const uint32_t rank = (uint32_t)rc.rank;
+  if (rc.dtype == EXD_F64) {
+    conserve_union_kernel<double><<<blocks, 256, 0, s>>>(
+        uni, counts, ncounts, static_cast<const double*>(contrib), static_cast<const double*>(e),
+        static_cast<const double*>(snap), bitmap, flag, rank);
+    conserve_rest_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(e),
+                                                        static_cast<const double*>(snap), bitmap,
+                                                        rc.n_g, flag, rank);
+  } else {
+    conserve_union_kernel<float><<<blocks, 256, 0, s>>>(
+        uni, counts, ncounts, static_cast<const float*>(contrib), static_cast<const float*>(e),
+        static_cast<const float*>(snap), bitmap, flag, rank);
+    conserve_rest_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(e),
+                                                       static_cast<const float*>(snap), bitmap,
+                                                       rc.n_g, flag, rank);
+  }
   return cudaGetLastError();
 }
 

@@ -32,14 +32,16 @@ class Pair:
     """B200 engine (in-process workers) + checker engine on identical inputs."""
 
     def __init__(self, cfg_kw, dtype="f32", segments=None, stream_seed=None, static=False,
-                 checker="oracle", verify_replication=True, distribution=0):
+                 checker="oracle", verify_replication=True, distribution=0,
+                 verify_conservation=False):
         import torch
         self.torch = torch
         self.cfg_kw = dict(cfg_kw)
         self.dtype = dtype
         self.cfg = S.SparsifierConfig(**cfg_kw)
         self.eng = S.Engine(self.cfg, S.EngineOptions(dtype=dtype, static_partitions=static,
-                                                       verify_replication=verify_replication))
+                                                       verify_replication=verify_replication,
+                                                       verify_conservation=verify_conservation))
         ocfg = O.make_config(**cfg_kw)
         if checker == "reference":
             self.chk = O.RefEngine(ocfg, O.make_options(static_partitions=int(static),

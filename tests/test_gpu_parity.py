@@ -322,3 +322,14 @@ def test_density_cap_fp64_vs_reference(kw):
         rec, orec = p.step(t)
         check_record(rec, orec, ctx=f"t={t}")
     p.compare_state(ctx="end")
+
+
+@pytest.mark.parametrize("kw", [CONFIGS[0], CONFIGS[2], CAP_CONFIGS[1], CONFIGS[7]],
+                         ids=lambda k: f"n{k['n']}_g{k['n_g']}")
+def test_verify_conservation_holds(kw):
+    """engine.cpp:221-249 on the device: every step's contributions equal the
+    acc snapshot at the union, the union is cleared, nothing else moves."""
+    p = Pair(kw, "f32", verify_conservation=True)
+    for t in range(8):
+        rec, orec = p.step(t)
+        check_record(rec, orec, ctx=f"t={t}")
