@@ -234,6 +234,7 @@ struct exd_engine {
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [2] local gate words
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
+  unsigned long long* rep_hash = nullptr;  // [4 * (n + 1)]: own words, then all ranks' words
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
   // profiling
@@ -419,6 +420,7 @@ void teardown(exd_engine* h) {
   for (void* p : h->peer_regions)
     if (p) cudaIpcCloseMemHandle(p);
   if (h->p2p) cudaFree(h->region);
+  cudaFree(h->rep_hash);
   cudaFree(h->d_slot);
   cudaFree(h->d_p2p_lists);
   cudaFree(h->d_push);
@@ -814,6 +816,16 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       CU(launch_verify_replication(h->w[0].ctrl, h->w[i].ctrl, h->w[0].x, h->w[i].x, c.n_g,
                                    h->opt.dtype, h->w[i].rank, h->verify_flag_dev, h->stream));
     h->stats.kernel_launches += nl - 1;
+    h->verify_t = h->t;
+  }
+  // verify_replication across ranks: hash, all-gather, compare with rank 0
+  if (h->opt.verify_replication && h->dist && n > 1) {
+    if (!h->rep_hash) CU(cudaMalloc((void**)&h->rep_hash, sizeof(unsigned long long) * 4 * (n + 1)));
+    Worker& wk = h->w[0];
+    CU(launch_replica_hash(wk.ctrl, wk.x, h->rep_hash, wk.rc, h->stream));
+    NC(nccl().AllGather(h->rep_hash, h->rep_hash + 4, 4, ncclUint64, h->comm, h->stream));
+    CU(launch_replica_compare(h->rep_hash + 4, n, h->verify_flag_dev, h->stream));
+    h->stats.kernel_launches += 2;
     h->verify_t = h->t;
   }
   h->t += 1;

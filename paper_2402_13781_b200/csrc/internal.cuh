@@ -174,6 +174,10 @@ struct CapArgs {
   int32_t npush;
 };
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s);
+cudaError_t launch_replica_hash(const Ctrl* c, const void* x, unsigned long long* out4, RunConst rc,
+                                cudaStream_t s);
+cudaError_t launch_replica_compare(const unsigned long long* all4, int n, uint32_t* flag,
+                                   cudaStream_t s);
 cudaError_t launch_snapshot(const void* e, const void* g, void* snap, RunConst rc, cudaStream_t s);
 cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int ncounts,
                                 const void* contrib, const void* e, const void* snap,

@@ -1331,6 +1331,54 @@ __global__ void verify_kernel(const Ctrl* c0, const Ctrl* cw, const T* x0, const
   if (bits) atomicCAS(flag, 0u, ((uint32_t)w << 8) | bits);
 }
 
+__host__ __device__ inline unsigned long long mix64(unsigned long long z);
+
+// ---- verify_replication across ranks (engine.cpp:251-272) --------------------
+// Replicas live on different GPUs: each rank hashes its replicated state per
+// field (delta bits, k_t, topology, x) into 4 words; the words are all-gathered
+// and compared against rank 0's. XOR of per-element mixes is order-free, so the
+// hash is deterministic whatever the reduction order.
+__device__ __forceinline__ unsigned long long mix_word(unsigned long long v, unsigned long long i) {
+  return mix64(v ^ (i * 0x9e3779b97f4a7c15ULL));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) replica_hash_kernel(const Ctrl* c, const T* x, int64_t n_g,
+                                                           int n, unsigned long long* out4) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long hd = mix_word((unsigned long long)__double_as_longlong(c->delta), 0);
+    unsigned long long hk = 0, ht = mix_word((unsigned long long)c->topo.sz_blk, 1);
+    for (int r = 0; r < n; ++r) {
+      hk ^= mix_word((unsigned long long)c->k_t[r], 2 + r);
+      ht ^= mix_word((unsigned long long)c->topo.blk_part[r], 100 + r);
+      ht ^= mix_word((unsigned long long)c->topo.blk_pos[r], 200 + r);
+    }
+    atomicXor(&out4[0], hd);
+    atomicXor(&out4[1], hk);
+    atomicXor(&out4[2], ht);
+  }
+  unsigned long long hx = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_g;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long b = sizeof(T) == 4 ? (unsigned long long)__float_as_uint((float)x[j])
+                                                : (unsigned long long)__double_as_longlong((double)x[j]);
+    hx ^= mix_word(b, (unsigned long long)j + 1000);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hx ^= __shfl_xor_sync(0xffffffffu, hx, o);
+  if ((threadIdx.x & 31) == 0 && hx) atomicXor(&out4[3], hx);
+}
+
+__global__ void replica_compare_kernel(const unsigned long long* all4, int n, uint32_t* flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int r = 1; r < n; ++r)
+    for (int f = 0; f < 4; ++f)  // reference order: delta, k_t, topology, x
+      if (all4[4 * r + f] != all4[f]) {
+        atomicCAS(flag, 0u, ((uint32_t)r << 8) | (1u << f));
+        return;
+      }
+}
+
 // ---- verify_conservation (engine.cpp:221-249), debug option -----------------
 // snapshot: acc = e + eta*g with the stream kernel's exact arithmetic, taken
 // before the step; after it: every contribution equals the snapshot at its
@@ -1585,6 +1633,26 @@ cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int 
                                                        static_cast<const float*>(snap), bitmap,
                                                        rc.n_g, flag, rank);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replica_hash(const Ctrl* c, const void* x, unsigned long long* out4, RunConst rc,
+                                cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(out4, 0, 4 * sizeof(unsigned long long), s);
+  if (err != cudaSuccess) return err;
+  const int blocks = grid_for(rc.n_g, 256 * 8);
+  if (rc.dtype == EXD_F64)
+    replica_hash_kernel<double><<<blocks, 256, 0, s>>>(c, static_cast<const double*>(x), rc.n_g, rc.n,
+                                                       out4);
+  else
+    replica_hash_kernel<float><<<blocks, 256, 0, s>>>(c, static_cast<const float*>(x), rc.n_g, rc.n,
+                                                      out4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replica_compare(const unsigned long long* all4, int n, uint32_t* flag,
+                                   cudaStream_t s) {
+  replica_compare_kernel<<<1, 32, 0, s>>>(all4, n, flag);
   return cudaGetLastError();
 }
 

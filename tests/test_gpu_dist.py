@@ -1,0 +1,46 @@
+"""GPU, >= 2 devices: one rank per GPU (torchrun), both collective paths, vs
+the oracle (tools/dist_check.py). Skipped on a single-GPU box."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _run(nproc, *args, port=29577):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tools", "dist_check.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "PASS" in r.stdout
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["p2p", "nccl"])
+def test_two_ranks_bit_exact_vs_oracle(sync):
+    _run(2, "--sync", sync, "--steps", "12")
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_two_ranks_density_cap():
+    _run(2, "--sync", "p2p", "--cap", "0.01", "--steps", "10", port=29578)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["p2p", "nccl"])
+def test_replica_divergence_detected_across_gpus(sync):
+    _run(2, "--sync", sync, "--inject", "1", port=29579)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_p2p_rank_order_sum_is_bit_exact():
+    _run(4, "--sync", "p2p", "--steps", "12", port=29580)

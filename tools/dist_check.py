@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--skew", type=int, default=1)
     ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p"])
     ap.add_argument("--cap", type=float, default=None, help="max_density_cap")
+    ap.add_argument("--inject", type=int, default=0,
+                    help="perturb x on rank 1 after step 2; the next step must raise EngineError "
+                         "(test_engine.cpp:219-226 across GPUs)")
     args = ap.parse_args()
 
     import numpy as np
@@ -53,6 +56,27 @@ def main():
     orc = O.OracleEngine(O.make_config(**kw), np.float32) if rank == 0 else None
     tmp = torch.empty(args.n_g, device=f"cuda:{local}")
     ok = True
+    if args.inject:
+        msg = ""
+        try:
+            for t in range(5):
+                src.gradient(t, rank, buf, "f32", eng.stream())
+                torch.cuda.synchronize()
+                eng.step([buf])
+                if t == 2 and rank == 1:
+                    x = eng.x(0)
+                    x[3] += 1.0
+                    eng.write(0, "x", x)
+        except S.EngineError as err:
+            msg = str(err)
+        good = msg == "replicated state diverged at iteration 3: rank 1 field x"
+        flags = [None] * world
+        dist.all_gather_object(flags, (good, msg))
+        if rank == 0:
+            print(f"dist_check world={world} sync={args.sync} inject: "
+                  f"{'PASS' if all(f[0] for f in flags) else 'FAIL'} {flags}", flush=True)
+        dist.destroy_process_group()
+        sys.exit(0 if all(f[0] for f in flags) else 1)
     for t in range(args.steps):
         src.gradient(t, rank, buf, "f32", eng.stream())
         torch.cuda.synchronize()
