@@ -68,10 +68,31 @@ EXD_HD void rotate(const int64_t* k_rank, int64_t t, int n, int64_t* k_part) {
   for (int i = 0; i < n; ++i) k_part[(shift + i) % n] = k_rank[i];
 }
 
+// rotate with t-1 already reduced mod n (the device keeps t mod n): the same
+// mapping with 32-bit arithmetic and no division
+EXD_HD void rotate_m(const int64_t* k_rank, int shift, int n, int64_t* k_part) {
+  for (int i = 0; i < n; ++i) {
+    int j = shift + i;
+    if (j >= n) j -= n;
+    k_part[j] = k_rank[i];
+  }
+}
+
 // adjust_topology, allocator.cpp:40-90 (Alg. 3): one left-to-right sweep of
-// adjacent-pair block migrations; later pairs see updated counts.
+// adjacent-pair block migrations; later pairs see updated counts. `inv_alpha`
+// is 1.0 / alpha, precomputed (the same IEEE quotient on host and device).
+EXD_HD void adjust_r(exd_topology& topo, int64_t* k, double alpha, double inv_alpha,
+                     int64_t blk_move, int64_t min_blk, int64_t n_g, int32_t* moves,
+                     int32_t* skips);
+
 EXD_HD void adjust(exd_topology& topo, int64_t* k, double alpha, int64_t blk_move,
                    int64_t min_blk, int64_t n_g, int32_t* moves, int32_t* skips) {
+  adjust_r(topo, k, alpha, ddiv(1.0, alpha), blk_move, min_blk, n_g, moves, skips);
+}
+
+EXD_HD void adjust_r(exd_topology& topo, int64_t* k, double alpha, double inv_alpha,
+                     int64_t blk_move, int64_t min_blk, int64_t n_g, int32_t* moves,
+                     int32_t* skips) {
   const int n = topo.n;
   *moves = 0;
   *skips = 0;
@@ -81,7 +102,6 @@ EXD_HD void adjust(exd_topology& topo, int64_t* k, double alpha, int64_t blk_mov
   const double pk_prev = ddiv((double)total, (double)n);
   const double den_prev = ddiv((double)total, (double)n_g);
   const int64_t k_move = llround_d(dmul((double)(blk_move * topo.sz_blk), den_prev));
-  const double inv_alpha = ddiv(1.0, alpha);
   for (int i = 0; i + 1 < n; ++i) {
     const double det = ddiv((double)k[i], pk_prev);
     const double det2 = ddiv((double)k[i + 1], pk_prev);
@@ -121,20 +141,34 @@ EXD_HD int allocate(const exd_topology& t, int64_t it, int rank, int64_t n_g, in
   return p;
 }
 
+// allocate with t reduced mod n (device): (t % n + rank) % n without division
+EXD_HD int allocate_m(const exd_topology& t, int tmod, int rank, int64_t n_g, int64_t* st,
+                      int64_t* end) {
+  int p = tmod + rank;
+  if (p >= t.n) p -= t.n;
+  partition_range(t, p, n_g, st, end);
+  return p;
+}
+
 // scale_threshold, threshold.cpp:23-35 (Alg. 5). `1.0 + 0.25*gamma` must not
-// be contracted into an FMA.
-EXD_HD double scale_threshold(int64_t k, int64_t k_prime, double delta, double beta,
-                              double gamma) {
+// be contracted into an FMA. `inv_beta` is 1.0 / beta, precomputed.
+EXD_HD double scale_threshold_r(int64_t k, int64_t k_prime, double delta, double beta,
+                                double inv_beta, double gamma) {
   const double exam = ddiv((double)k_prime, (double)k);
   double sf;
   if (exam > beta) {
     sf = dadd(1.0, gamma);
-  } else if (exam > ddiv(1.0, beta)) {
+  } else if (exam > inv_beta) {
     sf = dadd(1.0, dmul(0.25, gamma));
   } else {
     sf = dadd(1.0, -gamma);
   }
   return dmul(delta, sf);
+}
+
+EXD_HD double scale_threshold(int64_t k, int64_t k_prime, double delta, double beta,
+                              double gamma) {
+  return scale_threshold_r(k, k_prime, delta, beta, ddiv(1.0, beta), gamma);
 }
 
 // all_gather accounting, collectives.cpp:29-45 (Eqs. 2-5)

@@ -337,6 +337,8 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     rc.static_partitions = opt->static_partitions;
     rc.dtype = opt->dtype;
     rc.cap = h->cap;
+    rc.inv_alpha = 1.0 / cfg.alpha;
+    rc.inv_beta = 1.0 / cfg.beta;
     rc.fused = (n == 1 && h->cap == 0) ? 1 : 0;
     blk_magic(topo0.sz_blk, &rc.blk_magic, &rc.blk_shift);
     if (int r = alloc_zero(&wk.x, h->esz * ng)) return r;
@@ -372,6 +374,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     Ctrl c;
     std::memset(&c, 0, sizeof(c));
     c.t = 0;
+    c.tmod = 0;
     c.delta = cfg.has_delta0 ? cfg.delta0 : 0.0;
     c.has_delta = cfg.has_delta0;
     c.thr_f = cfg.has_delta0 ? round_up_float(cfg.delta0) : 0.0f;

@@ -28,6 +28,8 @@ struct Ctrl {
   double delta;             // selection threshold (fp64, as the reference)
   float thr_f;              // __double2float_ru(delta): fp32 compare key
   int32_t has_delta;        // delta known (delta0 given or estimated)
+  int32_t tmod;             // t mod n (keeps the epilogue free of 64-bit division)
+  int32_t reserved_tm;
   int64_t k_t[EXD_MAX_WORKERS];  // last gathered counts, rank order
   exd_topology topo;        // committed topology (reference's WorkerState::topology)
   Plan plan[2];             // plan of step t lives in plan[t & 1]: the epilogue
@@ -62,6 +64,7 @@ struct RunConst {
   int32_t blk_shift;
   int32_t fused;                 // n == 1 without a cap: x update + epilogue in the finish kernel
   int64_t cap;                   // per-rank density cap (engine.cpp:166-171); 0 = none
+  double inv_alpha, inv_beta;    // 1/alpha, 1/beta (host IEEE quotients, identical on device)
 };
 
 struct SelectArgs {

@@ -36,8 +36,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define PROBE(i) \
   do { if (threadIdx.x == 0) g_probe[i] = gtimer(); } while (0)
+#define PROBE_ANY(i) do { g_probe[i] = gtimer(); } while (0)
 #else
 #define PROBE(i) do {} while (0)
+#define PROBE_ANY(i) do {} while (0)
 #endif
 
 namespace {
@@ -137,20 +139,22 @@ __device__ __forceinline__ void copy_topo(exd_topology* dst, const exd_topology*
 
 // plan of step t_next from the topology committed by step t_next-1 and the
 // counts gathered at step t_next-1 (rank order)
+// (`kp` is shared-memory scratch: a local array would live in local memory,
+// where every first touch of the dependent chain is an L2 round trip)
 __device__ __noinline__ void make_plan(Plan* p, const exd_topology* base, const int64_t* k_rank,
-                                       int64_t t_next, const RunConst& rc) {
+                                       int tm_next, const RunConst& rc, int64_t* kp) {
+  // tm_next = t_next mod n; rotate's shift is (t_next - 1) mod n
   const int n = rc.n;
   copy_topo(&p->topo, base, n);
   int32_t mv = 0, sk = 0;
   if (!rc.static_partitions) {
-    int64_t kp[EXD_MAX_WORKERS];
-    rotate(k_rank, t_next, n, kp);
-    adjust(p->topo, kp, rc.alpha, rc.blk_move, rc.min_blk, rc.n_g, &mv, &sk);
+    rotate_m(k_rank, tm_next == 0 ? n - 1 : tm_next - 1, n, kp);
+    adjust_r(p->topo, kp, rc.alpha, rc.inv_alpha, rc.blk_move, rc.min_blk, rc.n_g, &mv, &sk);
   }
   p->moves = mv;
   p->skips = sk;
   int64_t st, end;
-  p->partition = allocate(p->topo, t_next, rc.rank, rc.n_g, &st, &end);
+  p->partition = allocate_m(p->topo, tm_next, rc.rank, rc.n_g, &st, &end);
   p->st = st;
   p->end = end;
 }
@@ -196,7 +200,7 @@ __device__ __noinline__ void advance_delta(Ctrl* c, const int64_t* k_rank, const
     kp += k_rank[r];
     c->k_t[r] = k_rank[r];
   }
-  c->delta = scale_threshold(rc.k, kp, c->delta, rc.beta, rc.gamma);
+  c->delta = scale_threshold_r(rc.k, kp, c->delta, rc.beta, rc.inv_beta, rc.gamma);
   c->thr_f = thr_of(c->delta);
   const Plan* cur = &c->plan[c->t & 1];
   copy_topo(&c->topo, &cur->topo, n);
@@ -207,6 +211,7 @@ __device__ __noinline__ void advance_delta(Ctrl* c, const int64_t* k_rank, const
   c->last.moves = cur->moves;
   c->last.skips = cur->skips;
   c->t += 1;
+  c->tmod = c->tmod + 1 == n ? 0 : c->tmod + 1;
 }
 
 // Shared-memory staging of the control block for one CTA.
@@ -216,6 +221,7 @@ struct EpiShared {
   int64_t k_rank[EXD_MAX_WORKERS];
   double norm2[EXD_MAX_WORKERS];
   int64_t capped[EXD_MAX_WORKERS];
+  int64_t scratch[EXD_MAX_WORKERS];  // make_plan's partition-order counts
 };
 
 __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
@@ -233,15 +239,19 @@ __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const Run
                                               exd_record* rec_out) {
   const int tid = threadIdx.x;
   const int64_t t = sh.c.t;
+  const int tm_next = sh.c.tmod + 1 == rc.n ? 0 : sh.c.tmod + 1;
   const double delta_used = sh.c.delta;
-  __syncthreads();  // everyone read t / delta before warp 0 changes them
+  __syncthreads();  // everyone read t / tmod / delta before warp 0 changes them
   if (tid == 0) {
     advance_delta(&sh.c, sh.k_rank, rc);
     sh.c.done = 0;
+    PROBE_ANY(26);
   } else if (tid == 32) {
-    make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, t + 1, rc);
+    make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc, sh.scratch);
+    PROBE_ANY(27);
   } else if (tid == 64 && rec_out) {
     make_record(&sh.rec, sh.k_rank, sh.norm2, sh.capped, t, delta_used, &sh.c.plan[t & 1], rc);
+    PROBE_ANY(28);
   }
   __syncthreads();
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);

@@ -24,7 +24,8 @@ for i in range(300):
 eng.sync()
 names = {0: "epi_start", 1: "epi_sums", 2: "epi_pre_cta", 4: "epi_ctrl_loaded", 5: "epi_computed",
          3: "epi_end", 8: "copy0_start", 9: "copy0_base", 10: "copyL_base", 11: "copy0_end",
-         12: "copyL_end", 16: "k1_first_cta", 17: "k1_last_cta"}
+         12: "copyL_end", 16: "k1_first_cta", 17: "k1_last_cta", 26: "epi_delta", 27: "epi_plan",
+         28: "epi_record"}
 rows = []
 for i in range(5):
     S.flush_l2(0, eng.stream())
