@@ -188,7 +188,8 @@ struct Worker {
   void* snapshot = nullptr;           // verify_conservation: acc of the running step
   uint32_t* bitmap = nullptr;         // verify_conservation: union membership
   exd_record* rec_host = nullptr;     // pinned: last record copied back at sync
-  exd_record* rec_dev = nullptr;      // device ring of kRecRing records (slot t % kRecRing)
+  RawRecord* rec_dev = nullptr;       // device ring of kRecRing raw records (slot t % kRecRing)
+  RawRecord* raw_host = nullptr;      // pinned: last raw record copied back at sync
   Plan plan0{};                       // host copy of the t = 0 plan
 };
 
@@ -368,7 +369,8 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     }
     CU(cudaHostAlloc((void**)&wk.rec_host, sizeof(exd_record), cudaHostAllocDefault));
     std::memset(wk.rec_host, 0, sizeof(exd_record));
-    if (int r = alloc_zero((void**)&wk.rec_dev, sizeof(exd_record) * kRecRing)) return r;
+    if (int r = alloc_zero((void**)&wk.rec_dev, sizeof(RawRecord) * kRecRing)) return r;
+    CU(cudaHostAlloc((void**)&wk.raw_host, sizeof(RawRecord), cudaHostAllocDefault));
 
     // engine.cpp:68-87: x = 0, e = 0, topology, k_t = k/n, delta = delta0
     Ctrl c;
@@ -451,6 +453,7 @@ void teardown(exd_engine* h) {
     if (h->dist && h->n > 1) cudaFree(wk.cnt);
     cudaFreeHost(wk.rec_host);
     cudaFree(wk.rec_dev);
+    cudaFreeHost(wk.raw_host);
   }
   cudaFree(h->counts_all);
   cudaFreeHost(h->counts_host);
@@ -608,6 +611,7 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.idx = wk.idx;
   a.val = wk.val;
   a.blk_counts = wk.blk + (h->t & 1) * h->cfg.n_b;
+  a.blk_next = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;
   a.stage = wk.stage;
   a.chunk_count = wk.chunk_count;
   a.tile_count = wk.tile_count;
@@ -633,9 +637,6 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   for (int i = 0; i < nl; ++i)
     if (!grads || !grads[i]) return set_err(EXD_EINVAL, "null gradient pointer");
   CU(cudaSetDevice(h->device));
-  // zero the other parity's block counters for the next step
-  for (auto& wk : h->w)
-    CU(cudaMemsetAsync(wk.blk + ((h->t + 1) & 1) * c.n_b, 0, 4 * (size_t)c.n_b, h->stream));
 
   // verify_conservation (engine.cpp:142): acc snapshot of every worker
   if (h->opt.verify_conservation) {
@@ -837,6 +838,37 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   return EXD_OK;
 }
 
+// IterationRecord of one step (collectives.cpp:29-45, engine.cpp:327-349) from
+// the device's raw record, with the reference's formulas (host side of
+// control.cuh, compiled without FMA contraction).
+void finalize_record(const RawRecord& r, const exd_config& cfg, exd_record* rec) {
+  const int n = r.n;
+  double norm_sum = 0.0;
+  for (int i = 0; i < n; ++i) norm_sum += std::sqrt(r.norm2[i]);
+  exd_gather_stats gs;
+  gather_stats(r.k_rank, n, &gs);
+  std::memset(rec, 0, sizeof(*rec));
+  rec->t = r.t;
+  rec->k_prime = gs.k_prime;
+  rec->density = (double)gs.k_prime / (double)cfg.n_g;
+  const int64_t diff = cfg.k - gs.k_prime;
+  rec->eps = (double)(diff < 0 ? -diff : diff) / (double)cfg.n_g;
+  rec->m_t = gs.m_t;
+  rec->c_t = gs.c_t;
+  rec->f_t = gs.f_t;
+  rec->global_err = norm_sum / (double)n;
+  rec->delta = r.delta;
+  rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
+  rec->union_count = gs.k_prime;
+  rec->n = n;
+  rec->adjust_moves = r.moves;
+  rec->adjust_skips = r.skips;
+  int cap_hits = 0;  // engine.cpp:345
+  for (int i = 0; i < n; ++i) cap_hits += r.capped[i] ? 1 : 0;
+  rec->cap_hits = cap_hits;
+  for (int i = 0; i < n; ++i) rec->k_rank[i] = r.k_rank[i];
+}
+
 int sync_engine(exd_engine* h, exd_record* out) {
   CU(cudaSetDevice(h->device));
   CU(cudaStreamSynchronize(h->stream));
@@ -878,9 +910,11 @@ int sync_engine(exd_engine* h, exd_record* out) {
     return set_err(EXD_EINVARIANT, msg);
   }
   if (h->has_record) {
-    for (auto& wk : h->w)
-      CU(cudaMemcpy(wk.rec_host, wk.rec_dev + ((h->t - 1) % kRecRing), sizeof(exd_record),
+    for (auto& wk : h->w) {
+      CU(cudaMemcpy(wk.raw_host, wk.rec_dev + ((h->t - 1) % kRecRing), sizeof(RawRecord),
                     cudaMemcpyDeviceToHost));
+      finalize_record(*wk.raw_host, h->cfg, wk.rec_host);
+    }
   }
   if (out) {
     if (!h->has_record) std::memset(out, 0, sizeof(*out));

@@ -44,6 +44,20 @@ struct Ctrl {
   double norm2;             // ||e_entering||^2 of the running step
 };
 
+// The device half of one ledger row (IterationRecord, engine.cpp:327-349): what
+// the step produced. The host turns it into the exd_record at sync
+// (finalize_record, engine.cu) with the reference's formulas, so the device
+// epilogue only does the control work the next step needs.
+struct RawRecord {
+  int64_t t;
+  double delta;                       // threshold the step selected with
+  int32_t moves, skips;               // AdjustStats of the step's plan
+  int32_t n, reserved;
+  int64_t k_rank[EXD_MAX_WORKERS];    // gathered counts, rank order
+  double norm2[EXD_MAX_WORKERS];      // ||e_entering||^2 per rank
+  int64_t capped[EXD_MAX_WORKERS];    // the density cap trimmed that rank
+};
+
 // What each rank contributes to the count all-gather (32 bytes).
 struct CountRec {
   int64_t k;
@@ -74,6 +88,7 @@ struct SelectArgs {
   int32_t* idx;             // [cap]    own selection, ascending
   void* val;                // T[cap]   own selected values
   int32_t* blk_counts;      // [n_b]    per-block selection counts
+  int32_t* blk_next;        // [n_b]    block counters of step t + 1 (zeroed by the finish kernel)
   void* stage;              // [cap + 2 tiles] (index, value) pairs: warp-chunk staging runs
   int32_t* chunk_count;     // [tiles * kChunksPerTile] selected per warp chunk
   int32_t* tile_count;      // [tiles + 4] selected per tile (<= tile size)
@@ -81,7 +96,7 @@ struct SelectArgs {
   double* cta_norm;         // [kMaxCtas] finish-kernel partials
   Ctrl* ctrl;
   CountRec* cnt_out;        // this rank's slot of the count all-gather
-  exd_record* rec;          // fused n == 1: record (mapped host memory)
+  RawRecord* rec;           // fused n == 1: this step's raw record
   int32_t tile_base;        // first tile covered by the stream launch
   int32_t num_tiles;        // tiles covered by the stream launch
   int64_t t;                // the step these kernels run (selects plan[t & 1])
@@ -110,7 +125,7 @@ struct FinalizeArgs {
   void* x;
   Ctrl* ctrl;
   const CountRec* counts;       // [n]
-  exd_record* rec;              // record (mapped host memory)
+  RawRecord* rec;               // this step's raw record
 };
 
 // ---- NVLink peer-memory sync (one rank per GPU, no host in the loop) --------
@@ -140,7 +155,7 @@ struct P2PArgs {
   CountRec* counts_all;              // [n] local copy of the gathered counts
   const CountRec* own_cnt;           // the finish kernel's {k_i, ||e||^2}
   Ctrl* ctrl;
-  exd_record* rec;
+  RawRecord* rec;
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
   unsigned long long* gate;          // [2] local gates: count / contrib epoch seen by block 0

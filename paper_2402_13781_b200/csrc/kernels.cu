@@ -37,7 +37,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PROBE(i) \
   do { if (threadIdx.x == 0) g_probe[i] = gtimer(); } while (0)
 #define PROBE_ANY(i) do { g_probe[i] = gtimer(); } while (0)
+#define PROBE_MAX(i) do { if (threadIdx.x == 0) atomicMax(&g_probe[i], gtimer()); } while (0)
+__device__ unsigned long long g_cta[4][2048];
+#define CPROBE(i, c) do { if (threadIdx.x == 0 && (c) < 2048) g_cta[i][c] = gtimer(); } while (0)
+#define CPROBE_V(i, c, v) do { if (threadIdx.x == 0 && (c) < 2048) g_cta[i][c] = (v); } while (0)
 #else
+#define CPROBE(i, c) do {} while (0)
+#define CPROBE_V(i, c, v) do {} while (0)
+#define PROBE_MAX(i) do {} while (0)
 #define PROBE(i) do {} while (0)
 #define PROBE_ANY(i) do {} while (0)
 #endif
@@ -120,14 +127,15 @@ __device__ __forceinline__ double fabs_t(double v) { return fabs(v); }
 
 // ---- control epilogue ----------------------------------------------------
 // The end of step t, once the gathered counts are known:
-//   record  the ledger row (collectives.cpp:29-45, engine.cpp:327-349)
 //   delta   threshold rescale, k_t update, topology commit (engine.cpp:206-213)
 //   plan    step t+1's rotate -> adjust -> allocate (engine.cpp:125-131)
-// It is sequential O(n) fp64/int64 work (IEEE divisions, 64-bit modulo) with
-// long dependency chains, so one CTA stages the control block in shared
-// memory (prefetched while the CTA's totals are still loading) and runs the
-// three independent parts on three different warps concurrently; step t+1's
-// plan goes to the other plan slot, so nothing else has to wait.
+//   record  the raw ledger row; the host derives the reference's
+//           IterationRecord from it at sync (engine.cpp:327-349)
+// It is sequential O(n) fp64 work with long dependency chains, so one CTA
+// stages the control block in shared memory (prefetched while the CTA's
+// totals are still loading) and runs delta and plan on two warps
+// concurrently; step t+1's plan goes to the other plan slot, so nothing else
+// has to wait.
 __device__ __forceinline__ void copy_topo(exd_topology* dst, const exd_topology* src, int n) {
   dst->n = src->n;
   dst->sz_blk = src->sz_blk;
@@ -147,7 +155,7 @@ __device__ __noinline__ void make_plan(Plan* p, const exd_topology* base, const 
   const int n = rc.n;
   copy_topo(&p->topo, base, n);
   int32_t mv = 0, sk = 0;
-  if (!rc.static_partitions) {
+  if (!rc.static_partitions && n > 1) {  // one partition: no pairs to adjust
     rotate_m(k_rank, tm_next == 0 ? n - 1 : tm_next - 1, n, kp);
     adjust_r(p->topo, kp, rc.alpha, rc.inv_alpha, rc.blk_move, rc.min_blk, rc.n_g, &mv, &sk);
   }
@@ -157,40 +165,6 @@ __device__ __noinline__ void make_plan(Plan* p, const exd_topology* base, const 
   p->partition = allocate_m(p->topo, tm_next, rc.rank, rc.n_g, &st, &end);
   p->st = st;
   p->end = end;
-}
-
-__device__ __noinline__ void make_record(exd_record* rec, const int64_t* k_rank,
-                                         const double* norm2, const int64_t* capped, int64_t t,
-                                         double delta_used, const Plan* cur, const RunConst& rc) {
-  const int n = rc.n;
-  double norm_sum = 0.0;
-  for (int r = 0; r < n; ++r) norm_sum = __dadd_rn(norm_sum, sqrt(norm2[r]));
-  exd_gather_stats gs;
-  gather_stats(k_rank, n, &gs);
-  rec->t = t;
-  rec->k_prime = gs.k_prime;
-  rec->density = __ddiv_rn((double)gs.k_prime, (double)rc.n_g);
-  const int64_t diff = rc.k - gs.k_prime;
-  rec->eps = __ddiv_rn((double)(diff < 0 ? -diff : diff), (double)rc.n_g);
-  rec->m_t = gs.m_t;
-  rec->c_t = gs.c_t;
-  rec->f_t = gs.f_t;
-  rec->global_err = __ddiv_rn(norm_sum, (double)n);
-  rec->delta = delta_used;
-  rec->has_loss = 0;
-  rec->reserved0 = 0;
-  rec->loss = 0.0;
-  rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
-  rec->union_count = gs.k_prime;
-  rec->n = n;
-  rec->adjust_moves = cur->moves;
-  rec->adjust_skips = cur->skips;
-  int cap_hits = 0;  // engine.cpp:345
-  for (int r = 0; r < n; ++r) cap_hits += capped[r] ? 1 : 0;
-  rec->cap_hits = cap_hits;
-  rec->idle_workers = 0;
-  rec->reserved1 = 0;
-  for (int r = 0; r < n; ++r) rec->k_rank[r] = k_rank[r];
 }
 
 __device__ __noinline__ void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc) {
@@ -217,7 +191,6 @@ __device__ __noinline__ void advance_delta(Ctrl* c, const int64_t* k_rank, const
 // Shared-memory staging of the control block for one CTA.
 struct EpiShared {
   Ctrl c;
-  exd_record rec;
   int64_t k_rank[EXD_MAX_WORKERS];
   double norm2[EXD_MAX_WORKERS];
   int64_t capped[EXD_MAX_WORKERS];
@@ -225,7 +198,7 @@ struct EpiShared {
 };
 
 __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
-  static_assert(sizeof(Ctrl) % 8 == 0 && sizeof(exd_record) % 8 == 0, "word copies");
+  static_assert(sizeof(Ctrl) % 8 == 0, "word copies");
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
   const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(cg);
   constexpr int W = (int)(sizeof(Ctrl) / 8);
@@ -236,7 +209,7 @@ __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
 // Run the epilogue on the staged copy (sh.c, sh.k_rank, sh.norm2 filled;
 // caller synced), then write the control block and the record back. Whole CTA.
 __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const RunConst& rc,
-                                              exd_record* rec_out) {
+                                              RawRecord* rec_out) {
   const int tid = threadIdx.x;
   const int64_t t = sh.c.t;
   const int tm_next = sh.c.tmod + 1 == rc.n ? 0 : sh.c.tmod + 1;
@@ -250,24 +223,29 @@ __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const Run
     make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc, sh.scratch);
     PROBE_ANY(27);
   } else if (tid == 64 && rec_out) {
-    make_record(&sh.rec, sh.k_rank, sh.norm2, sh.capped, t, delta_used, &sh.c.plan[t & 1], rc);
-    PROBE_ANY(28);
+    const Plan& cur = sh.c.plan[t & 1];
+    rec_out->t = t;
+    rec_out->delta = delta_used;
+    rec_out->moves = cur.moves;
+    rec_out->skips = cur.skips;
+    rec_out->n = rc.n;
+    rec_out->reserved = 0;
   }
+  if (rec_out)
+    for (int r = tid; r < rc.n; r += blockDim.x) {
+      rec_out->k_rank[r] = sh.k_rank[r];
+      rec_out->norm2[r] = sh.norm2[r];
+      rec_out->capped[r] = sh.capped[r];
+    }
   __syncthreads();
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
   unsigned long long* gw = reinterpret_cast<unsigned long long*>(cg);
   for (int i = tid; i < (int)(sizeof(Ctrl) / 8); i += blockDim.x) gw[i] = sw[i];
-  if (rec_out) {
-    const unsigned long long* rs = reinterpret_cast<const unsigned long long*>(&sh.rec);
-    unsigned long long* rd = reinterpret_cast<unsigned long long*>(rec_out);
-    const int words = (int)((offsetof(exd_record, k_rank) + 8 * rc.n + 7) / 8);
-    for (int i = tid; i < words; i += blockDim.x) rd[i] = rs[i];
-  }
 }
 
 // Standalone form: load, run, store (finalize kernel, block 0).
 __device__ __forceinline__ void control_epilogue_cta(Ctrl* cg, const CountRec* counts,
-                                                     const RunConst& rc, exd_record* rec_out) {
+                                                     const RunConst& rc, RawRecord* rec_out) {
   __shared__ EpiShared sh;
   epi_load(sh, cg);
   for (int r = threadIdx.x; r < rc.n; r += blockDim.x) {
@@ -511,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
       a.tile_count[tile] = sc;
     }
   }
+  PROBE_MAX(31);
 }
 
 // ---- K2: the finish kernel ----------------------------------------------------
@@ -549,7 +528,13 @@ __device__ __forceinline__ int64_t cta_sum_counts(const int32_t* __restrict__ cn
   return t;
 }
 
-constexpr int kCopyUnroll = 4;
+#ifndef EXD_COPY_UNROLL
+#define EXD_COPY_UNROLL 8
+#endif
+#ifndef EXD_COPY_PER_SM
+#define EXD_COPY_PER_SM 2
+#endif
+constexpr int kCopyUnroll = EXD_COPY_UNROLL;  // staged entries in flight per thread
 
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst rc) {
@@ -579,6 +564,8 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     __shared__ EpiShared esh;
     if (FUSED) epi_load(esh, ctrl);  // the stream kernel never writes the control block
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // next step's block counters (nobody reads that parity during this step)
+    for (int i = tid; i < rc.n_b; i += kThreads) a.blk_next[i] = 0;
     // one round of wide independent loads for both totals
     const int nt = (int)((n_g + TILE - 1) / TILE);
     double pn = 0.0;
@@ -634,22 +621,24 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
       epi_run_store(esh, ctrl, rc, a.rec);
     }
     PROBE(3);
+    PROBE_MAX(30);
     return;
   }
 
   // ---- copy CTAs: a static contiguous range of the partition's tiles
   if (r == 0) PROBE(8);
+  CPROBE(0, r);
   const int ntp = lt - ft + 1;
+  const int64_t fc = st / CH;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's counts and runs
   const int t0 = ft + (int)(((int64_t)ntp * r) / G);
   const int t1 = ft + (int)(((int64_t)ntp * (r + 1)) / G);
-  const int64_t fc = st / CH;
-  const int nch = (t1 - t0) * kWarps;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's counts and runs
-  // chunk counts of the first batch, issued before the prefix sum (independent)
-  int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
   const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
+  const int nch = (t1 - t0) * kWarps;
+  int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
   if (r == 0) PROBE(9);
   if (r == G - 1) PROBE(10);
+  CPROBE(1, r);
 
   T* __restrict__ val = static_cast<T*>(a.val);
   T* __restrict__ x = static_cast<T*>(a.x);
@@ -720,6 +709,9 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   }
   if (r == 0) PROBE(11);
   if (r == G - 1) PROBE(12);
+  CPROBE(2, r);
+  CPROBE_V(3, r, (unsigned long long)(running - base));
+  PROBE_MAX(30);
 }
 
 template <typename T, bool UNIT>
@@ -746,7 +738,7 @@ cudaError_t launch_finish_t(const SelectArgs& a, const RunConst& rc, cudaStream_
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cap = sms * 2 > kMaxCtas ? kMaxCtas : sms * 2;
+    cap = sms * EXD_COPY_PER_SM > kMaxCtas ? kMaxCtas : sms * EXD_COPY_PER_SM;
   }
   // the partition's tile count is device-resident; size for the whole vector,
   // plus one epilogue CTA
@@ -1511,6 +1503,9 @@ static __global__ void l2_read_kernel(const float4* __restrict__ p, int64_t n4, 
 #ifdef EXD_PROBE
 extern "C" int exd_debug_probe(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_probe, sizeof(g_probe));
+}
+extern "C" int exd_debug_ctas(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_cta, sizeof(g_cta));
 }
 #endif
 

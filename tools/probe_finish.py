@@ -22,17 +22,25 @@ torch.cuda.synchronize()
 for i in range(300):
     eng.step_async(pool[i % 2])
 eng.sync()
-names = {0: "epi_start", 1: "epi_sums", 2: "epi_pre_cta", 4: "epi_ctrl_loaded", 5: "epi_computed",
+names = {4: "epi_warm", 0: "epi_start", 1: "epi_sums", 2: "epi_pre_cta",
          3: "epi_end", 8: "copy0_start", 9: "copy0_base", 10: "copyL_base", 11: "copy0_end",
          12: "copyL_end", 16: "k1_first_cta", 17: "k1_last_cta", 26: "epi_delta", 27: "epi_plan",
-         28: "epi_record"}
+         28: "epi_record", 30: "K2_END", 31: "K1_END"}
 rows = []
+xs = torch.cuda.ExternalStream(eng.stream())
 for i in range(5):
     S.flush_l2(0, eng.stream())
-    eng.step(pool[i % 2])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(xs)
+    eng.step_async(pool[i % 2])
+    e1.record(xs)
+    eng.sync()
     buf = (C.c_uint64 * 64)()
     L.exd_debug_probe(buf)
+    zero = (C.c_uint64 * 64)()
     t0 = buf[16]
-    rows.append({names[k]: (buf[k] - t0) / 1e3 for k in names if buf[k]})
+    row = {names[k]: (buf[k] - t0) / 1e3 for k in names if buf[k]}
+    row["EVENTS_us"] = e0.elapsed_time(e1) * 1e3
+    rows.append(row)
 for r in rows:
     print("  ".join(f"{k}={v:.1f}" for k, v in sorted(r.items(), key=lambda kv: kv[1])))
