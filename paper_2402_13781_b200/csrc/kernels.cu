@@ -280,6 +280,10 @@ template <> struct Pair<float> {
   __device__ static P make(uint32_t j, float v) { return make_uint2(j, __float_as_uint(v)); }
   __device__ static uint32_t idx(const P& p) { return p.x; }
   __device__ static float val(const P& p) { return __uint_as_float(p.y); }
+  __device__ static void store_keep(P* q, const P& p, uint64_t pol) {  // L2 evict_last
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(q), "r"(p.x), "r"(p.y),
+                 "l"(pol) : "memory");
+  }
 };
 template <> struct Pair<double> {
   using P = ulonglong2;
@@ -288,6 +292,10 @@ template <> struct Pair<double> {
   }
   __device__ static uint32_t idx(const P& p) { return (uint32_t)p.x; }
   __device__ static double val(const P& p) { return __longlong_as_double((long long)p.y); }
+  __device__ static void store_keep(P* q, const P& p, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(q), "l"(p.x), "l"(p.y),
+                 "l"(pol) : "memory");
+  }
 };
 
 template <typename V>
@@ -437,6 +445,8 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     const uint32_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
     const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
     const bool split = b_lo != b_hi;
+    uint64_t keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     typename Pair<T>::P* sp = static_cast<typename Pair<T>::P*>(a.stage);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -451,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
             const uint32_t j = lbeg + u * 32 * VN + c;
-            sp[pos] = Pair<T>::make(j, v[u][c]);
-#ifdef EXD_XP_X_PREFETCH
-            if (rc.n == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<T*>(a.x) + j));
-#endif
+            // the finish kernel reads the pair (and, n == 1, updates x[j])
+            // right after the stream: keep both in L2 past the streaming data
+            Pair<T>::store_keep(&sp[pos], Pair<T>::make(j, v[u][c]), keep);
+            if (rc.fused) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<T*>(a.x) + j));
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
             ++pos;
           }
