@@ -461,10 +461,9 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
             const uint32_t j = lbeg + u * 32 * VN + c;
-            // the finish kernel reads the pair (and, n == 1, updates x[j])
-            // right after the stream: keep both in L2 past the streaming data
+            // the finish kernel reads the pair right after the stream: keep
+            // it in L2 past the streaming data
             Pair<T>::store_keep(&sp[pos], Pair<T>::make(j, v[u][c]), keep);
-            if (rc.fused) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(static_cast<T*>(a.x) + j));
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
             ++pos;
           }
