@@ -233,7 +233,7 @@ struct exd_engine {
   void** d_contrib = nullptr;         // [2][n]
   unsigned int* p2p_err = nullptr;    // pinned host copy
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
-  unsigned long long* p2p_gate = nullptr;  // [2] local gate words
+  unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   unsigned long long* rep_hash = nullptr;  // [4 * (n + 1)]: own words, then all ranks' words
   int32_t* recv = nullptr;
@@ -561,7 +561,7 @@ int setup_p2p(exd_engine* h) {
   CU(cudaHostAlloc((void**)&h->p2p_err, sizeof(unsigned int), cudaHostAllocDefault));
   *h->p2p_err = 0;
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
-  if (int r2 = alloc_zero((void**)&h->p2p_gate, 2 * sizeof(unsigned long long))) return r2;
+  if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
   // barrier: every rank has mapped every peer before anyone steps
   int* d_b = nullptr;
   CU(cudaMalloc((void**)&d_b, sizeof(int)));
@@ -721,9 +721,8 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       pa.err = h->p2p_err_dev;
       pa.gate = h->p2p_gate;
       pa.me = wk.rank;
-      CU(launch_p2p_union(pa, wk.rc, h->stream));
-      CU(launch_p2p_reduce(pa, wk.rc, h->stream));
-      h->stats.kernel_launches += 2;
+      CU(launch_p2p_sync(pa, wk.rc, h->stream));
+      h->stats.kernel_launches += 1;
     } else if (h->dist && n > 1) {
       Worker& wk = h->w[0];
       NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));

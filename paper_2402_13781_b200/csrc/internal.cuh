@@ -158,7 +158,7 @@ struct P2PArgs {
   RawRecord* rec;
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
-  unsigned long long* gate;          // [2] local gates: count / contrib epoch seen by block 0
+  unsigned long long* gate;          // [3] local gates: count / contrib epoch seen by block 0, arrive counter
   int32_t me;
 };
 
@@ -200,8 +200,7 @@ cudaError_t launch_snapshot(const void* e, const void* g, void* snap, RunConst r
 cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int ncounts,
                                 const void* contrib, const void* e, const void* snap,
                                 uint32_t* bitmap, uint32_t* flag, RunConst rc, cudaStream_t s);
-cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s);
-cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s);
+cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
 

@@ -856,18 +856,19 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs a, RunConst 
 // no host in the loop and no padding:
 //   finish      (already running) also PUSHES this rank's ascending index list
 //               into its slot of every peer's inbox (posted NVLink stores).
-//   p2p_union   publishes {k_i, ||e||^2} + an epoch into every peer's inbox,
+//   p2p_sync    publishes {k_i, ||e||^2} + an epoch into every peer's inbox,
 //               waits on its OWN inbox (local polling), builds the union in
 //               partition order from the (now local) lists, gathers this rank's
-//               contributions, clears e at the union.
-//   p2p_reduce  publishes "contributions ready", waits, sums the contributions
-//               in RANK ORDER straight from the peers' buffers (bit-identical to
-//               all_reduce_sum, collectives.cpp:59-70, for every n), x -= g/n,
-//               control epilogue.
+//               contributions, clears e at the union; then (in-kernel arrive
+//               counter instead of a kernel boundary) publishes "contributions
+//               ready", waits, sums the contributions in RANK ORDER straight
+//               from the peers' buffers (bit-identical to all_reduce_sum,
+//               collectives.cpp:59-70, for every n), x -= g/n, and runs the
+//               control epilogue on a spare block.
 // Buffer reuse is safe without extra handshakes: a rank overwrites its list
-// slot / count in a peer's inbox only in step t+1, after its own p2p_reduce(t)
+// slot / count in a peer's inbox only in step t+1, after its own p2p_sync(t)
 // saw that peer's contrib epoch t+1 (published when the peer had finished
-// p2p_union(t)); contributions are double buffered by step parity.
+// phase A of p2p_sync(t)); contributions are double buffered by step parity.
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -940,13 +941,20 @@ __device__ bool wait_inbox(const PeerFlags* inbox, int n, bool contrib, unsigned
   return gv != ~0ull && *(volatile unsigned int*)err == 0;
 }
 
+// One kernel for both exchange rounds: phase A builds the union and this
+// rank's contributions, an in-kernel arrive counter replaces the kernel
+// boundary, phase B sums the peers' contributions. Every CTA is resident (the
+// grid is 2 per SM + 1 and the previous kernel retires), so the counter cannot
+// deadlock. The last block runs the control epilogue as soon as the counts are
+// in (it needs nothing else).
 template <typename T>
-__global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) {
+__global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
   __shared__ int64_t s_off[EXD_MAX_WORKERS + 1];
   __shared__ int32_t s_rank[EXD_MAX_WORKERS];
   __shared__ bool s_ok;
   const int n = rc.n, tid = threadIdx.x;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the finish kernel's list pushes
+  const int G = gridDim.x - 1;  // work blocks; block G: control epilogue
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the finish/cap kernel's list pushes
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (blockIdx.x == 0) PROBE(20);
   if (blockIdx.x == 0 && tid < n) {
@@ -964,6 +972,21 @@ __global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) 
   __syncthreads();
   if (blockIdx.x == 0) PROBE(21);
   if (!s_ok) return;
+  if ((int)blockIdx.x == G) {
+    // the counts of every rank are in the inbox (block 0 copies them to
+    // counts_all concurrently, so read the inbox itself)
+    __shared__ EpiShared esh;
+    epi_load(esh, a.ctrl);
+    for (int r = tid; r < n; r += blockDim.x) {
+      esh.k_rank[r] = __ldcg(&a.inbox[r].k);
+      esh.norm2[r] = __ldcg(&a.inbox[r].norm2);
+      esh.capped[r] = __ldcg(&a.inbox[r].capped);
+    }
+    __syncthreads();
+    epi_run_store(esh, a.ctrl, rc, a.rec);
+    PROBE(24);
+    return;
+  }
   if (tid == 0) {
     const int64_t tm = mod_floor(a.ctrl->t, n);
     int64_t off = 0;
@@ -982,98 +1005,104 @@ __global__ void __launch_bounds__(256) p2p_union_kernel(P2PArgs a, RunConst rc) 
   }
   __syncthreads();
   const int64_t kp = s_off[n];
-  T* e = static_cast<T*>(a.e);
-  T* c = static_cast<T*>(a.contrib[a.me]);
-  const T* own = static_cast<const T*>(a.own_val);
-  const T* xx = static_cast<const T*>(a.x);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // 4 entries per thread in flight: list reads, then residual reads, then writes
-  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 4 * stride) {
-    int32_t j[4];
-    int r4[4];
-    int64_t loc[4];
+  {
+    // ---- phase A: union in partition order, own contributions, clear e
+    T* e = static_cast<T*>(a.e);
+    T* c = static_cast<T*>(a.contrib[a.me]);
+    const T* own = static_cast<const T*>(a.own_val);
+    const T* xx = static_cast<const T*>(a.x);
+    const int64_t stride = (int64_t)G * blockDim.x;
+    // 4 entries per thread in flight: list reads, then residual reads, then writes
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 4 * stride) {
+      int32_t j[4];
+      int r4[4];
+      int64_t loc[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t pos = p0 + q * stride;
-      r4[q] = -1;
-      if (pos < kp) {
-        int p = 0;
-        while (p + 1 < n && s_off[p + 1] <= pos) ++p;
-        r4[q] = s_rank[p];
-        loc[q] = pos - s_off[p];
-        j[q] = __ldcg(&a.lists[r4[q]][loc[q]]);  // local: own list or pushed inbox slot
+      for (int q = 0; q < 4; ++q) {
+        const int64_t pos = p0 + q * stride;
+        r4[q] = -1;
+        if (pos < kp) {
+          int p = 0;
+          while (p + 1 < n && s_off[p + 1] <= pos) ++p;
+          r4[q] = s_rank[p];
+          loc[q] = pos - s_off[p];
+          j[q] = __ldcg(&a.lists[r4[q]][loc[q]]);  // local: own list or pushed inbox slot
+        }
+      }
+      T v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (r4[q] < 0) continue;
+        v[q] = r4[q] == a.me ? own[loc[q]] : e[j[q]];  // own residual already cleared
+        // phase B read-modify-writes x[j]: pull the line into L2 now
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(xx + j[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (r4[q] < 0) continue;
+        const int64_t pos = p0 + q * stride;
+        a.idx_global[pos] = j[q];
+        c[pos] = v[q];
+        if (r4[q] != a.me) e[j[q]] = T(0);
       }
     }
-    T v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (r4[q] < 0) continue;
-      v[q] = r4[q] == a.me ? own[loc[q]] : e[j[q]];  // own residual already cleared
-      // the reduce kernel read-modify-writes x[j]: pull the line into L2 now
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(xx + j[q]));
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (r4[q] < 0) continue;
-      const int64_t pos = p0 + q * stride;
-      a.idx_global[pos] = j[q];
-      c[pos] = v[q];
-      if (r4[q] != a.me) e[j[q]] = T(0);
-    }
   }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) p2p_reduce_kernel(P2PArgs a, RunConst rc) {
-  __shared__ bool s_ok;
-  const int n = rc.n, tid = threadIdx.x;
-  const int G = gridDim.x - 1;  // last block: control epilogue (needs only the counts)
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // our contributions are complete
-  if ((int)blockIdx.x == G) {
-    control_epilogue_cta(a.ctrl, a.counts_all, rc, a.rec);
-    PROBE(24);
-    return;
+  // ---- every work block's contributions are written: block 0 announces
+  // "contributions ready" (one system fence), waits for the peers', opens gate 1
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(&a.gate[2], 1ull);
   }
-  if (blockIdx.x == 0) PROBE(22);
-  if (blockIdx.x == 0 && tid < n) {
-    asm volatile("fence.acq_rel.sys;" ::: "memory");  // our contributions (previous kernel)
-    st_relaxed_sys(&a.peer_slot[tid]->contrib_epoch, a.epoch);
+  if (blockIdx.x == 0) {
+    if (tid == 0) {
+      const unsigned long long want = a.epoch * (unsigned long long)G;
+      while (*(volatile unsigned long long*)&a.gate[2] < want) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    PROBE(22);
+    if (tid < n) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      st_relaxed_sys(&a.peer_slot[tid]->contrib_epoch, a.epoch);
+    }
   }
   if (tid == 0) s_ok = wait_inbox(a.inbox, n, true, a.epoch, &a.gate[1], a.err);
   __syncthreads();
   if (blockIdx.x == 0) PROBE(23);
   if (!s_ok) return;
-  int64_t kp = 0;
-  for (int r = 0; r < n; ++r) kp += a.counts_all[r].k;
-  T* x = static_cast<T*>(a.x);
-  T* g = static_cast<T*>(a.sum);
-  const int64_t stride = (int64_t)G * blockDim.x;
-  const int nn = n < 8 ? n : 8;
-  // 2 entries per thread in flight: every peer's contribution for both, then x
-  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 2 * stride) {
-    T v[2][8];
-    int32_t j[2];
+  {
+    // ---- phase B: rank-order sum straight from the peers' buffers, x -= g/n
+    T* x = static_cast<T*>(a.x);
+    T* g = static_cast<T*>(a.sum);
+    const int64_t stride = (int64_t)G * blockDim.x;
+    const int nn = n < 8 ? n : 8;
+    // 2 entries per thread in flight: every peer's contribution for both, then x
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + tid; p0 < kp; p0 += 2 * stride) {
+      T v[2][8];
+      int32_t j[2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int64_t pos = p0 + q * stride;
-      if (pos < kp) {
-        for (int r = 0; r < nn; ++r) v[q][r] = __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
-        j[q] = a.idx_global[pos];
+      for (int q = 0; q < 2; ++q) {
+        const int64_t pos = p0 + q * stride;
+        if (pos < kp) {
+          for (int r = 0; r < nn; ++r) v[q][r] = __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
+          j[q] = a.idx_global[pos];
+        }
       }
-    }
-    T xv[2];
+      T xv[2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (p0 + q * stride < kp) xv[q] = x[j[q]];
+      for (int q = 0; q < 2; ++q)
+        if (p0 + q * stride < kp) xv[q] = x[j[q]];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int64_t pos = p0 + q * stride;
-      if (pos >= kp) continue;
-      T s = v[q][0];  // rank order, as all_reduce_sum (collectives.cpp:62-68)
-      for (int r = 1; r < nn; ++r) s += v[q][r];
-      for (int r = 8; r < n; ++r) s += __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
-      g[pos] = s;
-      x[j[q]] = apply_update<T>(xv[q], s, n);
+      for (int q = 0; q < 2; ++q) {
+        const int64_t pos = p0 + q * stride;
+        if (pos >= kp) continue;
+        T sv = v[q][0];  // rank order, as all_reduce_sum (collectives.cpp:62-68)
+        for (int r = 1; r < nn; ++r) sv += v[q][r];
+        for (int r = 8; r < n; ++r) sv += __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
+        g[pos] = sv;
+        x[j[q]] = apply_update<T>(xv[q], sv, n);
+      }
     }
   }
   if (blockIdx.x == 0) PROBE(25);
@@ -1594,16 +1623,10 @@ static cudaError_t launch_pdl(K kernel, int blocks, cudaStream_t s, const P2PArg
   return cudaLaunchKernelEx(&cfg, kernel, a, rc);
 }
 
-cudaError_t launch_p2p_union(const P2PArgs& a, RunConst rc, cudaStream_t s) {
-  const int blocks = p2p_blocks();
-  if (rc.dtype == EXD_F64) return launch_pdl(p2p_union_kernel<double>, blocks, s, a, rc);
-  return launch_pdl(p2p_union_kernel<float>, blocks, s, a, rc);
-}
-
-cudaError_t launch_p2p_reduce(const P2PArgs& a, RunConst rc, cudaStream_t s) {
+cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s) {
   const int blocks = p2p_blocks() + 1;
-  if (rc.dtype == EXD_F64) return launch_pdl(p2p_reduce_kernel<double>, blocks, s, a, rc);
-  return launch_pdl(p2p_reduce_kernel<float>, blocks, s, a, rc);
+  if (rc.dtype == EXD_F64) return launch_pdl(p2p_sync_kernel<double>, blocks, s, a, rc);
+  return launch_pdl(p2p_sync_kernel<float>, blocks, s, a, rc);
 }
 
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {

@@ -34,7 +34,7 @@ if hasattr(L, "exd_debug_probe"):
     L.exd_debug_probe.argtypes = [C.POINTER(C.c_uint64)]
     buf = (C.c_uint64 * 64)(); L.exd_debug_probe(buf)
     t0 = buf[16]
-    names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "gather", 21: "gather_waited", 22: "reduce", 23: "reduce_waited", 24: "reduce_epi_end", 25: "reduce_b0_end"}
+    names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "sync", 21: "counts_in", 22: "contrib_done", 23: "contribs_in", 24: "epi_end", 25: "b0_end"}
     out += "  | " + "  ".join(f"{v}={(buf[k]-t0)/1e3:.1f}" for k, v in sorted(names.items(), key=lambda kv: buf[kv[0]]) if buf[k])
 print(out, flush=True)
 dist.barrier(); dist.destroy_process_group()
