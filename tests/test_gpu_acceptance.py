@@ -1,0 +1,112 @@
+"""GPU: the reference's acceptance criteria for the ExDyna path, restated on
+the device engine (acceptance_main.cpp; the main run is n = 8 workers,
+n_g = 1M, d = 0.001, seed 7, 1000 iterations, default 4-segment stream).
+
+  C2 density tracking        acceptance_main.cpp:181-199
+  C7 threshold == top-k      acceptance_main.cpp:341-366
+  C8 ledger identities and
+     topology invariants     acceptance_main.cpp:369-414
+  C9 determinism             acceptance_main.cpp:417-428
+
+C4 (padding reduction) is in test_gpu_configs.py.
+"""
+import numpy as np
+import pytest
+
+from paper_2402_13781_b200 import sparsim as S
+
+pytestmark = pytest.mark.gpu
+
+MAIN = dict(n=8, n_g=1_000_000, d=0.001, seed=7)
+ITERS, WARMUP = 1000, 100
+
+
+def _run(iters, **kw):
+    import torch
+    cfg = S.SparsifierConfig(**kw)
+    eng = S.Engine(cfg, S.EngineOptions(verify_replication=False))
+    src = S.SyntheticStream(S.StreamSpec(n_g=cfg.n_g, seed=cfg.seed))
+    bufs = [torch.empty(cfg.n_g, device="cuda") for _ in range(cfg.n)]
+    recs = eng.run(iters, src, bufs)
+    return eng, recs
+
+
+@pytest.fixture(scope="module")
+def main_run():
+    eng, recs = _run(ITERS, **MAIN)
+    yield eng, recs
+    eng.close()
+
+
+def test_c2_density_tracking(main_run):
+    _, recs = main_run
+    d = MAIN["d"]
+    dens = np.array([r.density for r in recs[WARMUP:]])
+    mean = dens.mean()
+    band = np.mean((dens >= d / 2) & (dens <= 2 * d))
+    assert 0.75 * d <= mean <= 1.25 * d, mean / d
+    assert band >= 0.90, band
+
+
+def test_c8_ledger_identities_and_topology(main_run):
+    eng, recs = main_run
+    n, n_g = MAIN["n"], MAIN["n_g"]
+    k = S.validate(S.SparsifierConfig(**MAIN)).k
+    for r in recs:
+        kr = list(r.k_rank[:n])
+        s, m = sum(kr), max(kr)
+        assert r.k_prime == s and r.m_t == m
+        assert r.c_t == n * sum(m - c for c in kr)
+        assert s == 0 or r.f_t == n * float(m) / float(s)
+        assert r.eps == abs(k - s) / n_g  # density_error, engine.cpp:369-371
+        assert r.union_count == s and r.duplicates == 0
+    topo = eng.topology(0)
+    assert sum(topo.blk_part) == 256 and topo.blk_pos[0] == 0
+    for i in range(1, n):
+        assert topo.blk_pos[i] == topo.blk_pos[i - 1] + topo.blk_part[i - 1]
+    cursor = 0
+    for p in range(n):
+        r = S.partition_range(topo, p, n_g)
+        assert r.st == cursor
+        cursor = r.end
+    assert cursor == n_g
+    # every worker holds the same replicated control state
+    for w in range(1, n):
+        assert eng.delta(w) == eng.delta(0) and eng.k_t(w) == eng.k_t(0)
+        assert eng.topology(w).blk_part == topo.blk_part
+
+
+def test_c7_threshold_selection_equals_exact_topk():
+    """A threshold strictly between the k-th and (k+1)-th magnitude selects
+    exactly the top-k set (ties excluded by construction, as the reference)."""
+    import torch
+    n_g, k = 10_000, 100
+    rng = np.random.default_rng(2026)
+    agree = trials = 0
+    for _ in range(100):
+        acc = rng.laplace(0.0, 1.0, n_g).astype(np.float32)
+        mags = np.sort(np.abs(acc).astype(np.float64))[::-1]
+        kth, nxt = mags[k - 1], mags[k]
+        if kth == nxt:
+            continue
+        trials += 1
+        delta = nxt + (kth - nxt) / 2
+        cfg = S.SparsifierConfig(n=1, n_g=n_g, n_b=1, d=k / n_g, min_blk=1, delta0=delta)
+        with S.Engine(cfg, S.EngineOptions(verify_replication=False)) as eng:
+            g = torch.from_numpy(acc).cuda()  # e starts at 0 and eta = 1: acc = g
+            eng.step([g])
+            sel = eng.selection(0)
+        topk = np.sort(np.argsort(-np.abs(acc.astype(np.float64)), kind="stable")[:k]).astype(np.int32)
+        agree += int(np.array_equal(sel, topk))
+    assert trials >= 95 and agree == trials
+
+
+def test_c9_determinism_byte_identical_ledgers():
+    kw = dict(n=8, n_g=200_000, d=0.005, seed=1)
+    e1, r1 = _run(200, **kw)
+    e2, r2 = _run(200, **kw)
+    assert S.format_csv(r1) == S.format_csv(r2)
+    for w in (0, 7):
+        assert np.array_equal(e1.x(w), e2.x(w)) and np.array_equal(e1.e(w), e2.e(w))
+    e1.close()
+    e2.close()
