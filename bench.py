@@ -134,6 +134,19 @@ def max_over_ranks(values, dist=None):
 
 
 # ------------------------------------------------------- reference (CPU) ----
+def host_cpu():
+    """CPU model and core count of this host (for the baseline's context)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}, nproc={os.cpu_count()}"
+
+
 def reference_ms_per_step(n, steps, warmup, pool=None):
     """Time the unmodified reference's Engine::step() (oracle/_ref) on this host."""
     import numpy as np
@@ -177,8 +190,7 @@ def run_reference(args):
         "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"full R18 Engine::step() with {n} simulated workers, "
                                    f"{steps} timed steps after {warmup} warm-up "
-                                   f"(verify_replication on, worker threads on; host nproc="
-                                   f"{os.cpu_count()})"},
+                                   f"(verify_replication on, worker threads on; {host_cpu()})"},
         "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -345,7 +357,8 @@ def run_ours(args):
             cms, _ = reference_ms_per_step(1, 5, 1, pool=2)
             cpu = {"value": cms, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": "5 full R18 n=1 Engine::step() calls of the unmodified reference "
-                             "(oracle/_ref) after 1 warm-up, replayed fp32-rounded gradients"}
+                             "(oracle/_ref) after 1 warm-up, replayed fp32-rounded gradients; "
+                             + host_cpu()}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
