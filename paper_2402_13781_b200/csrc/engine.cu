@@ -178,7 +178,6 @@ struct Worker {
   void* stage = nullptr;              // warp-chunk staging of the compaction ((idx, val) pairs)
   int32_t* chunk_count = nullptr;
   int32_t* tile_count = nullptr;
-  double* cta_norm = nullptr;
   double* tile_norm = nullptr;
   Ctrl* ctrl = nullptr;
   CountRec* cnt = nullptr;            // this worker's count slot
@@ -351,7 +350,6 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero(&wk.stage, 2 * h->esz * stage_cap)) return r;
     if (int r = alloc_zero((void**)&wk.chunk_count, 4 * (size_t)(h->tiles + 1) * kChunksPerTile)) return r;
     if (int r = alloc_zero((void**)&wk.tile_count, 4 * (size_t)(h->tiles + 8))) return r;
-    if (int r = alloc_zero((void**)&wk.cta_norm, 8 * (size_t)kMaxCtas)) return r;
     if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
     if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
     if (opt->verify_conservation) {
@@ -442,7 +440,6 @@ void teardown(exd_engine* h) {
     cudaFree(wk.stage);
     cudaFree(wk.chunk_count);
     cudaFree(wk.tile_count);
-    cudaFree(wk.cta_norm);
     cudaFree(wk.tile_norm);
     cudaFree(wk.ctrl);
     cudaFree(wk.idx_global);
@@ -616,7 +613,6 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.chunk_count = wk.chunk_count;
   a.tile_count = wk.tile_count;
   a.tile_norm = wk.tile_norm;
-  a.cta_norm = wk.cta_norm;
   a.ctrl = wk.ctrl;
   a.cnt_out = wk.cnt;
   a.rec = wk.rec_dev + (h->t % kRecRing);

@@ -93,7 +93,6 @@ struct SelectArgs {
   int32_t* chunk_count;     // [tiles * kChunksPerTile] selected per warp chunk
   int32_t* tile_count;      // [tiles + 4] selected per tile (<= tile size)
   double* tile_norm;        // [tiles] ||e_entering||^2 partial per tile
-  double* cta_norm;         // [kMaxCtas] finish-kernel partials
   Ctrl* ctrl;
   CountRec* cnt_out;        // this rank's slot of the count all-gather
   RawRecord* rec;           // fused n == 1: this step's raw record
