@@ -284,6 +284,11 @@ def run_ours(args):
     recs.append(eng.sync())
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("EXD_BENCH_VERBOSE"):
+        srt = sorted(step_ms)
+        print(f"[rank {rank}] step ms: mean {statistics.mean(step_ms):.4f} min {srt[0]:.4f} "
+              f"median {srt[len(srt) // 2]:.4f} max {srt[-1]:.4f} first5 "
+              f"{[round(v, 4) for v in step_ms[:5]]}", file=sys.stderr, flush=True)
     ks = eng.kernel_stats()
     launches = ks["kernel_launches"] - launches0
     total_ms = sum(step_ms)
@@ -365,8 +370,10 @@ def run_ours(args):
 
     cfg_line = workload(n)
     if n > 1:
-        cfg_line["sync"] = ("NVLink peer-memory kernels (no host wait)" if eng.sync_mode() == "p2p"
-                            else "NCCL all-gather/all-reduce + one host wait")
+        cfg_line["sync"] = {
+            "p2p": "NVLink peer memory, owner-reduce (peer residuals read in place; no host wait)",
+            "p2p-pull": "NVLink peer memory, pull-reduce (lists pushed, contributions pulled)",
+            "nccl": "NCCL all-gather/all-reduce + one host wait"}[eng.sync_mode()]
     line = {
         "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
@@ -396,7 +403,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p"],
+    ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p", "p2p-pull"],
                     help="N > 1: NVLink peer-memory sync (auto/p2p) or the NCCL chain")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -11,7 +11,7 @@ NCCL_ID_BYTES = 128
 
 EXD_OK, EXD_EINVAL, EXD_EINVARIANT, EXD_ECUDA, EXD_ENCCL, EXD_ENOMEM, EXD_EUNSUPPORTED = range(7)
 EXD_F32, EXD_F64 = 0, 1
-EXD_SYNC_AUTO, EXD_SYNC_NCCL, EXD_SYNC_P2P = 0, 1, 2
+EXD_SYNC_AUTO, EXD_SYNC_NCCL, EXD_SYNC_P2P, EXD_SYNC_P2P_PULL = 0, 1, 2, 3
 EXD_SPARSIFIER_EXDYNA, EXD_SPARSIFIER_TOPK, EXD_SPARSIFIER_CLTK, EXD_SPARSIFIER_HARD_THRESHOLD = range(4)
 (EXD_VEC_X, EXD_VEC_E, EXD_VEC_IDX_GLOBAL, EXD_VEC_LOCAL_IDX, EXD_VEC_LOCAL_VAL,
  EXD_VEC_BLOCK_COUNTS, EXD_VEC_SUM) = range(7)

@@ -234,6 +234,14 @@ struct exd_engine {
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
+  // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
+  //   | chunk counts[2][n] | tile counts[2][n] | contrib words[n][n_g]   ([2]: step parity)
+  bool xchg = false;
+  std::vector<int32_t*> push_stage[2], push_chunk[2], push_tile[2];  // [n-1] my slots in every peer's inbox
+  std::vector<PeerFlags*> slot_host;                   // [n] my parity-0 flag slot in every rank's inbox
+  std::vector<const int32_t*> stage_in[2], chunk_in[2], tile_in[2];  // [n] inbox slots by source
+  std::vector<void*> contrib_out;                      // [n] my contribution slot in every inbox
+  std::vector<const void*> contrib_in;                 // [n] contribution slots by source (local)
   unsigned long long* rep_hash = nullptr;  // [4 * (n + 1)]: own words, then all ranks' words
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
@@ -494,18 +502,44 @@ int setup_p2p(exd_engine* h) {
   CU(cudaStreamSynchronize(h->stream));
   cudaFree(d_ok);
   if (!ok_all) {
-    if (h->opt.sync_mode == EXD_SYNC_P2P)
+    if (h->opt.sync_mode == EXD_SYNC_P2P || h->opt.sync_mode == EXD_SYNC_P2P_PULL)
       return set_err(EXD_EUNSUPPORTED, "EXD_SYNC_P2P: some peers are not P2P-reachable");
     return EXD_OK;
   }
-  // inbox layout: flags[n] | lists[n][cap_part] | contrib[2][n_g]
-  const size_t flags_b = ((sizeof(PeerFlags) * (size_t)n) + 255) & ~(size_t)255;
-  const size_t list_b = ((4 * (size_t)h->cap_part) + 255) & ~(size_t)255;
-  const size_t con_b = ((h->esz * (size_t)h->cfg.n_g) + 255) & ~(size_t)255;
-  const size_t off_lists = flags_b, off_c0 = off_lists + list_b * (size_t)n, off_c1 = off_c0 + con_b;
-  const size_t total = off_c1 + con_b;
+  // push-reduce unless the caller asked for pull-reduce, or a density cap /
+  // verify_conservation needs the trimmed lists and contribution buffers first
+  h->xchg = h->opt.sync_mode != EXD_SYNC_P2P_PULL && h->cap == 0 && !h->opt.verify_conservation;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  // flag slots: two step parities for push-reduce
+  const size_t flags_b = al(sizeof(PeerFlags) * (size_t)n * (h->xchg ? 2 : 1));
+  size_t list_b, con_b, off_lists, off_c0, off_c1, total;
+  size_t stage_b = 0, chunk_b = 0, tile_b = 0, xcon_b = 0, off_st = 0, off_ch = 0, off_ti = 0, off_xc = 0;
+  if (h->xchg) {
+    // push-reduce: flags[2][n] | stage idx[2][n] | chunk counts[2][n] | tile counts[2][n]
+    //              | contribution words[n] (8 B {value, epoch} per fp32 entry, 16 B per fp64)
+    stage_b = al(4 * ((size_t)h->cap_part + 2 * (size_t)h->tile));
+    chunk_b = al(4 * (size_t)(h->tiles + 1) * kChunksPerTile);
+    tile_b = al(4 * (size_t)(h->tiles + 8));
+    xcon_b = al(2 * h->esz * (size_t)h->cfg.n_g);
+    off_st = flags_b;
+    off_ch = off_st + stage_b * 2 * n;
+    off_ti = off_ch + chunk_b * 2 * n;
+    off_xc = off_ti + tile_b * 2 * n;
+    total = off_xc + xcon_b * n;
+    list_b = con_b = off_lists = off_c0 = off_c1 = 0;
+  } else {
+    // pull-reduce: flags[n] | lists[n][cap_part] | contrib[2][n_g]
+    list_b = al(4 * (size_t)h->cap_part);
+    con_b = al(h->esz * (size_t)h->cfg.n_g);
+    off_lists = flags_b;
+    off_c0 = off_lists + list_b * (size_t)n;
+    off_c1 = off_c0 + con_b;
+    total = off_c1 + con_b;
+  }
   CU(cudaMalloc(&h->region, total));
   CU(cudaMemset(h->region, 0, flags_b));
+  // contribution words start with epoch 0 (never a live epoch)
+  if (h->xchg) CU(cudaMemset(static_cast<char*>(h->region) + off_xc, 0, xcon_b * n));
   h->inbox = static_cast<PeerFlags*>(h->region);
   Worker& wk = h->w[0];
   cudaIpcMemHandle_t mine;
@@ -533,6 +567,33 @@ int setup_p2p(exd_engine* h) {
     h->peer_regions[r] = p;
     base[r] = static_cast<char*>(p);
   }
+  if (h->xchg) {
+    char* own = static_cast<char*>(h->region);
+    h->contrib_out.assign(n, nullptr);
+    h->contrib_in.assign(n, nullptr);
+    h->slot_host.assign(n, nullptr);
+    for (int par = 0; par < 2; ++par) {
+      h->stage_in[par].assign(n, nullptr);
+      h->chunk_in[par].assign(n, nullptr);
+      h->tile_in[par].assign(n, nullptr);
+      for (int r = 0; r < n; ++r) {
+        if (r == me) continue;
+        // my slots in rank r's inbox, and rank r's slots in mine
+        const size_t sm = (size_t)(par * n + me), sr = (size_t)(par * n + r);
+        h->push_stage[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_st + stage_b * sm));
+        h->push_chunk[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_ch + chunk_b * sm));
+        h->push_tile[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_ti + tile_b * sm));
+        h->stage_in[par][r] = reinterpret_cast<const int32_t*>(own + off_st + stage_b * sr);
+        h->chunk_in[par][r] = reinterpret_cast<const int32_t*>(own + off_ch + chunk_b * sr);
+        h->tile_in[par][r] = reinterpret_cast<const int32_t*>(own + off_ti + tile_b * sr);
+      }
+    }
+    for (int r = 0; r < n; ++r) {
+      h->contrib_out[r] = base[r] + off_xc + xcon_b * me;
+      h->contrib_in[r] = own + off_xc + xcon_b * r;
+      h->slot_host[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
+    }
+  }
   std::vector<PeerFlags*> slot(n);
   std::vector<const int32_t*> lists(n);
   std::vector<int32_t*> push;
@@ -542,11 +603,11 @@ int setup_p2p(exd_engine* h) {
     slot[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
     lists[r] = r == me ? wk.idx : reinterpret_cast<const int32_t*>(own + off_lists + list_b * r);
     if (r != me) push.push_back(reinterpret_cast<int32_t*>(base[r] + off_lists + list_b * me));
-    con[r] = base[r] + off_c0;
-    con[n + r] = base[r] + off_c1;
+    con[r] = h->xchg ? nullptr : base[r] + off_c0;
+    con[n + r] = h->xchg ? nullptr : base[r] + off_c1;
   }
-  h->p2p_own_contrib[0] = own + off_c0;
-  h->p2p_own_contrib[1] = own + off_c1;
+  h->p2p_own_contrib[0] = h->xchg ? nullptr : own + off_c0;
+  h->p2p_own_contrib[1] = h->xchg ? nullptr : own + off_c1;
   CU(cudaMalloc((void**)&h->d_slot, sizeof(void*) * n));
   CU(cudaMalloc((void**)&h->d_p2p_lists, sizeof(void*) * n));
   CU(cudaMalloc((void**)&h->d_push, sizeof(void*) * (n > 1 ? n - 1 : 1)));
@@ -572,7 +633,8 @@ int setup_p2p(exd_engine* h) {
 
 // K1 (stream) and, unless accumulate-only, K2 (finish); CUDA events around
 // each when profiling so the bench can report the stream kernel's own time.
-int select_phase(exd_engine* h, int mode, const SelectArgs& a, const RunConst& rc) {
+int select_phase(exd_engine* h, int mode, const SelectArgs& a, const RunConst& rc,
+                 const ExchangeArgs* xa = nullptr) {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   const bool prof = h->opt.profile_kernels != 0;
   if (prof) {
@@ -590,7 +652,9 @@ int select_phase(exd_engine* h, int mode, const SelectArgs& a, const RunConst& r
   h->stats.kernel_launches += 1;
   if (prof) CU(cudaEventRecord(ev[1], h->stream));
   if (mode != kAccumulate) {
-    CU(launch_finish(a, rc, h->stream));
+    // push-reduce: the finish work and the whole sync are one kernel
+    if (xa) CU(launch_exchange(*xa, rc, h->stream));
+    else CU(launch_finish(a, rc, h->stream));
     h->stats.kernel_launches += 1;
   }
   if (prof) {
@@ -620,9 +684,42 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.num_tiles = (int32_t)h->tiles;
   a.t = h->t;
   // with a cap the list is pushed only after it is trimmed (cap kernel)
-  a.push_idx = (h->p2p && h->cap == 0) ? h->d_push : nullptr;
-  a.npush = (h->p2p && h->cap == 0) ? h->n - 1 : 0;
+  a.push_idx = (h->p2p && !h->xchg && h->cap == 0) ? h->d_push : nullptr;
+  a.npush = (h->p2p && !h->xchg && h->cap == 0) ? h->n - 1 : 0;
+  a.k1_npush = h->xchg ? h->n - 1 : 0;
+  const int par = (int)(h->t & 1);  // this step's parity slots
+  for (int q = 0; q < a.k1_npush; ++q) {
+    a.push_stage[q] = h->push_stage[par][q];
+    a.push_chunk[q] = h->push_chunk[par][q];
+    a.push_tile[q] = h->push_tile[par][q];
+  }
   return a;
+}
+
+ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
+  Worker& wk = h->w[0];
+  ExchangeArgs o{};
+  o.s = sa;
+  o.inbox = h->inbox;
+  for (int r = 0; r < h->n; ++r) {
+    o.peer_slot[r] = h->slot_host[r];
+    for (int par = 0; par < 2; ++par) {
+      o.stage_in[par][r] = h->stage_in[par][r];
+      o.chunk_in[par][r] = h->chunk_in[par][r];
+      o.tile_in[par][r] = h->tile_in[par][r];
+    }
+    o.contrib_out[r] = h->contrib_out[r];
+    o.contrib_in[r] = h->contrib_in[r];
+  }
+  o.idx_global = wk.idx_global;
+  o.sum = h->sum;
+  o.counts_all = h->counts_all;
+  o.rec = wk.rec_dev + (h->t % kRecRing);
+  o.epoch = (unsigned long long)h->t + 1;
+  o.err = h->p2p_err_dev;
+  o.gate = h->p2p_gate;
+  o.me = wk.rank;
+  return o;
 }
 
 // Engine::step, engine.cpp:274-350, enqueued on the engine's stream.
@@ -668,12 +765,14 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       const int64_t last = (wk.plan0.end - 1) / h->tile;
       a.tile_base = (int32_t)first;
       a.num_tiles = (int32_t)(last - first + 1);
-      if (int r = select_phase(h, kSelectOnly, a, wk.rc)) return r;
+      const ExchangeArgs xa = h->xchg ? exchange_args(h, a) : ExchangeArgs{};
+      if (int r = select_phase(h, kSelectOnly, a, wk.rc, h->xchg ? &xa : nullptr)) return r;
     }
   } else {
     for (int i = 0; i < nl; ++i) {
       SelectArgs a = select_args(h, h->w[i], grads[i]);
-      if (int r = select_phase(h, kFused, a, h->w[i].rc)) return r;
+      const ExchangeArgs xa = h->xchg ? exchange_args(h, a) : ExchangeArgs{};
+      if (int r = select_phase(h, kFused, a, h->w[i].rc, h->xchg ? &xa : nullptr)) return r;
     }
   }
 
@@ -695,7 +794,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
     }
   }
 
-  if (h->union_flow) {
+  if (h->union_flow && !h->xchg) {
     if (h->dist && n > 1 && h->p2p) {
       // f1: peer-memory sync, no host wait, no NCCL
       Worker& wk = h->w[0];
@@ -1093,7 +1192,7 @@ int32_t exd_engine_local_workers(const exd_engine* h) { return (int32_t)h->w.siz
 int32_t exd_engine_first_rank(const exd_engine* h) { return h->w.empty() ? 0 : h->w[0].rank; }
 int64_t exd_engine_iteration(const exd_engine* h) { return h->t; }
 int32_t exd_engine_sync_mode(const exd_engine* h) {
-  return !h->dist ? -1 : (h->p2p ? EXD_SYNC_P2P : EXD_SYNC_NCCL);
+  return !h->dist ? -1 : !h->p2p ? EXD_SYNC_NCCL : h->xchg ? EXD_SYNC_P2P : EXD_SYNC_P2P_PULL;
 }
 void* exd_engine_stream(const exd_engine* h, int32_t) { return (void*)h->stream; }
 

@@ -99,8 +99,14 @@ struct SelectArgs {
   int32_t tile_base;        // first tile covered by the stream launch
   int32_t num_tiles;        // tiles covered by the stream launch
   int64_t t;                // the step these kernels run (selects plan[t & 1])
-  int32_t* const* push_idx;  // P2P: [n] my list slot in every peer's inbox (nullptr: none)
+  int32_t* const* push_idx;  // P2P pull: [n] my list slot in every peer's inbox (nullptr: none)
   int32_t npush;
+  // P2P push-reduce: the stream kernel's pushes into every peer's inbox (by
+  // value: kernel parameters are constant-bank reads, no pointer round trip)
+  int32_t* push_stage[EXD_MAX_WORKERS - 1];  // [k1_npush] my staged-index slot
+  int32_t* push_chunk[EXD_MAX_WORKERS - 1];  // [k1_npush] my per-chunk count slot
+  int32_t* push_tile[EXD_MAX_WORKERS - 1];   // [k1_npush] my per-tile count slot
+  int32_t k1_npush;             // 0: no pushes
 };
 
 constexpr int kMaxCtas = 2048;
@@ -138,7 +144,8 @@ struct PeerFlags {                   // inbox[src] on the receiver
   double norm2;
   unsigned long long contrib_epoch;  // src's contributions of step epoch-1 are readable
   int64_t capped;
-  unsigned long long pad[11];        // 128 B: one slot per line
+  int64_t st, end;                   // src's partition range of step epoch-1 (push-reduce)
+  unsigned long long pad[9];         // 128 B: one slot per line
 };
 
 struct P2PArgs {
@@ -158,6 +165,32 @@ struct P2PArgs {
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
   unsigned long long* gate;          // [3] local gates: count / contrib epoch seen by block 0, arrive counter
+  int32_t me;
+};
+
+// Push-reduce step (one rank per GPU, no density cap): replaces the finish
+// kernel + p2p_sync. The stream kernel pushes its staged indices and counts
+// into the peers' inboxes; the exchange kernel builds the union from them,
+// pushes this rank's contributions into every inbox (coalesced posted stores)
+// and sums the n local contribution slots in rank order.
+struct ExchangeArgs {
+  SelectArgs s;                      // the stream kernel's outputs, own idx/val, x, e, ctrl
+  PeerFlags* inbox;                  // [2][n] own inbox flag slots by step parity (local)
+  // pointer tables by value (constant bank)
+  PeerFlags* peer_slot[EXD_MAX_WORKERS];        // my parity-0 flag slot in every rank's inbox
+  // [step parity][source rank]: pushed staged-index runs / per-chunk / per-tile counts (local)
+  const int32_t* stage_in[2][EXD_MAX_WORKERS];
+  const int32_t* chunk_in[2][EXD_MAX_WORKERS];
+  const int32_t* tile_in[2][EXD_MAX_WORKERS];
+  void* contrib_out[EXD_MAX_WORKERS];           // my {value, epoch} slot in every rank's inbox
+  const void* contrib_in[EXD_MAX_WORKERS];      // {value, epoch} slots by source rank (local)
+  int32_t* idx_global;               // [k'] union, partition order
+  void* sum;                         // [k'] aggregated values (T)
+  CountRec* counts_all;              // [n] local copy of the gathered counts
+  RawRecord* rec;
+  unsigned long long epoch;          // t + 1
+  unsigned int* err;                 // set on a peer timeout (device memory)
+  unsigned long long* gate;          // [3] local gate words ([0]: H1 seen)
   int32_t me;
 };
 
@@ -200,6 +233,7 @@ cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int 
                                 const void* contrib, const void* e, const void* snap,
                                 uint32_t* bitmap, uint32_t* flag, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s);
+cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
 

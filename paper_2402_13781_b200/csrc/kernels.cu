@@ -313,7 +313,9 @@ __device__ __forceinline__ uint32_t block_of(uint32_t j, const RunConst& rc) {
   return b < (uint32_t)(rc.n_b - 1) ? b : (uint32_t)(rc.n_b - 1);
 }
 
-template <typename T, int MODE, bool UNIT>
+// PUSH (one rank per GPU, push-reduce sync): the staged indices and the
+// per-chunk / per-tile counts of the partition also go to every peer's inbox.
+template <typename T, int MODE, bool UNIT, bool PUSH>
 __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArgs a, RunConst rc) {
   constexpr int VN = Vec<T>::N;
   constexpr int CH = chunk_of<T>();
@@ -322,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
   static_assert(CH * kWarps == tile_of<T>(), "tile = kWarps chunks");
   __shared__ double s_norm[kWarps];
   __shared__ int s_cnt[kWarps];
+  // PUSH: each warp's run of staged indices, copied to the peers coalesced
+  __shared__ int32_t s_run[PUSH ? kWarps * CH : 1];
 
   const Ctrl* ctrl = a.ctrl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -464,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
             // the finish kernel reads the pair right after the stream: keep
             // it in L2 past the streaming data
             Pair<T>::store_keep(&sp[pos], Pair<T>::make(j, v[u][c]), keep);
+            if (PUSH) s_run[warp * CH + (pos - sbase)] = (int32_t)j;
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
             ++pos;
           }
@@ -472,7 +477,17 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
       running += (int)(__popc(b0) + 2u * __popc(b1) + 4u * __popc(b2));
     }
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
+    if (PUSH && running) {
+      // the run sbase + [0, running) in every peer's staging slot: 128 B stores
+      __syncwarp();
+      for (int q = 0; q < a.k1_npush; ++q) {
+        int32_t* dst = a.push_stage[q] + sbase;
+        for (int i = lane; i < running; i += 32) dst[i] = s_run[warp * CH + i];
+      }
+    }
   }
+  constexpr int TILE = tile_of<T>();
+  const bool push_tile = PUSH && (uint32_t)tile >= st / TILE && (uint32_t)tile <= (end - 1) / TILE;
   if (SELECT && lane == 0) a.chunk_count[tile * kWarps + warp] = running;
 #ifdef EXD_XP_NO_TILE
   return;
@@ -496,6 +511,18 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) sc += s_cnt[w];
       a.tile_count[tile] = sc;
+      if (push_tile) {
+        // the tile's kWarps chunk counts as two 16 B stores, then its count
+        static_assert(kWarps == 8, "two int4 per tile");
+        const int4 c0 = make_int4(s_cnt[0], s_cnt[1], s_cnt[2], s_cnt[3]);
+        const int4 c1 = make_int4(s_cnt[4], s_cnt[5], s_cnt[6], s_cnt[7]);
+        for (int q = 0; q < a.k1_npush; ++q) {
+          int4* d = reinterpret_cast<int4*>(a.push_chunk[q] + tile * kWarps);
+          d[0] = c0;
+          d[1] = c1;
+          a.push_tile[q][tile] = sc;
+        }
+      }
     }
   }
   PROBE_MAX(31);
@@ -723,12 +750,18 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   PROBE_MAX(30);
 }
 
+template <typename T, bool UNIT, bool PUSH>
+void launch_stream_p(int mode, const SelectArgs& a, const RunConst& rc, cudaStream_t s) {
+  const dim3 grid(a.num_tiles), block(kThreads);
+  if (mode == kFused) stream_kernel<T, kFused, UNIT, PUSH><<<grid, block, 0, s>>>(a, rc);
+  else if (mode == kAccumulate) stream_kernel<T, kAccumulate, UNIT, false><<<grid, block, 0, s>>>(a, rc);
+  else stream_kernel<T, kSelectOnly, UNIT, PUSH><<<grid, block, 0, s>>>(a, rc);
+}
+
 template <typename T, bool UNIT>
 void launch_stream_u(int mode, const SelectArgs& a, const RunConst& rc, cudaStream_t s) {
-  const dim3 grid(a.num_tiles), block(kThreads);
-  if (mode == kFused) stream_kernel<T, kFused, UNIT><<<grid, block, 0, s>>>(a, rc);
-  else if (mode == kAccumulate) stream_kernel<T, kAccumulate, UNIT><<<grid, block, 0, s>>>(a, rc);
-  else stream_kernel<T, kSelectOnly, UNIT><<<grid, block, 0, s>>>(a, rc);
+  if (a.k1_npush > 0) launch_stream_p<T, UNIT, true>(mode, a, rc, s);
+  else launch_stream_p<T, UNIT, false>(mode, a, rc, s);
 }
 
 template <typename T>
@@ -909,26 +942,30 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned l
 // system-scope acquire fence once everyone is in, then opens a local gate word
 // for the other blocks. Gives up after 20 s (sets `err`) so a dead peer cannot
 // hang the GPU. Call from thread 0; returns false on timeout.
-__device__ bool wait_inbox(const PeerFlags* inbox, int n, bool contrib, unsigned long long epoch,
-                           unsigned long long* gate, unsigned int* err) {
+__device__ bool poll_inbox_open_gate(const PeerFlags* inbox, int n, bool contrib,
+                                     unsigned long long epoch, unsigned long long* gate,
+                                     unsigned int* err) {
   const unsigned long long t0 = gtime_ns();
-  if (blockIdx.x == 0) {
-    for (int r = 0; r < n; ++r) {
-      const unsigned long long* w = contrib ? &inbox[r].contrib_epoch : &inbox[r].count_epoch;
-      unsigned spins = 0;
-      while (ld_relaxed_sys(w) < epoch) {
-        if ((++spins & 255u) == 0 && gtime_ns() - t0 > 20000000000ull) {
-          atomicExch(err, 1u);
-          st_release_gpu(gate, ~0ull);  // release the other blocks, they see err
-          return false;
-        }
-        __nanosleep(20);
+  for (int r = 0; r < n; ++r) {
+    const unsigned long long* w = contrib ? &inbox[r].contrib_epoch : &inbox[r].count_epoch;
+    unsigned spins = 0;
+    while (ld_relaxed_sys(w) < epoch) {
+      if ((++spins & 255u) == 0 && gtime_ns() - t0 > 20000000000ull) {
+        atomicExch(err, 1u);
+        st_release_gpu(gate, ~0ull);  // release the other blocks, they see err
+        return false;
       }
+      __nanosleep(20);
     }
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    st_release_gpu(gate, epoch);
-    return true;
   }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  st_release_gpu(gate, epoch);
+  return true;
+}
+
+__device__ bool wait_gate(const unsigned long long* gate, unsigned long long epoch,
+                          unsigned int* err) {
+  const unsigned long long t0 = gtime_ns();
   unsigned spins = 0;
   unsigned long long gv;
   while ((gv = ld_acquire_gpu(gate)) < epoch) {
@@ -939,6 +976,12 @@ __device__ bool wait_inbox(const PeerFlags* inbox, int n, bool contrib, unsigned
     __nanosleep(20);
   }
   return gv != ~0ull && *(volatile unsigned int*)err == 0;
+}
+
+__device__ bool wait_inbox(const PeerFlags* inbox, int n, bool contrib, unsigned long long epoch,
+                           unsigned long long* gate, unsigned int* err) {
+  if (blockIdx.x == 0) return poll_inbox_open_gate(inbox, n, contrib, epoch, gate, err);
+  return wait_gate(gate, epoch, err);
 }
 
 // One kernel for both exchange rounds: phase A builds the union and this
@@ -1085,7 +1128,9 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
       for (int q = 0; q < 2; ++q) {
         const int64_t pos = p0 + q * stride;
         if (pos < kp) {
-          for (int r = 0; r < nn; ++r) v[q][r] = __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (r < nn) v[q][r] = __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
           j[q] = a.idx_global[pos];
         }
       }
@@ -1098,7 +1143,9 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
         const int64_t pos = p0 + q * stride;
         if (pos >= kp) continue;
         T sv = v[q][0];  // rank order, as all_reduce_sum (collectives.cpp:62-68)
-        for (int r = 1; r < nn; ++r) sv += v[q][r];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+          if (r < nn) sv += v[q][r];
         for (int r = 8; r < n; ++r) sv += __ldcg(&static_cast<const T*>(a.contrib[r])[pos]);
         g[pos] = sv;
         x[j[q]] = apply_update<T>(xv[q], sv, n);
@@ -1106,6 +1153,367 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
     }
   }
   if (blockIdx.x == 0) PROBE(25);
+}
+
+// ---- f1, push-reduce: the whole sync in the kernel after the stream ---------
+// One rank per GPU, no density cap. Replaces finish + p2p_sync with ONE kernel,
+// ONE cross-GPU handshake, and only posted NVLink stores (no remote reads):
+//   K1  (stream_kernel<..., PUSH>) besides staging its (index, value) pairs
+//       locally, copies each warp's run of staged indices and the per-chunk /
+//       per-tile counts of its partition into its slots of every peer's inbox
+//       (slots double-buffered by step parity).
+//   H1  block 0 totals this rank's counts once K1 is complete and publishes
+//       {k_i, ||e||^2, partition range} + epoch into every rank's inbox (one
+//       system fence also covers K1's pushes).
+//   A+B every work block owns one contiguous segment of ONE partition's union
+//       positions (collectives.cpp:47-55: the union is the concatenation of the
+//       ascending lists in partition order), located from the holder's chunk /
+//       tile counts exactly as the finish kernel does. Per entry, one thread:
+//       gathers its own contribution acc[j] (engine.cpp:310-317), stores it
+//       into every peer's inbox as a 64-bit {value, epoch} word (the low-latency
+//       protocol: the word is its own flag, so no fence and no second
+//       handshake), clears e[j] (selector.cpp:63-65), then polls the peers'
+//       words for the same position, sums the n contributions in rank order
+//       (all_reduce_sum, collectives.cpp:62-68: bit-identical for every n) and
+//       applies x -= g/n (engine.cpp:215). Every rank runs the same position
+//       split, so a position's n contributions are produced at about the same
+//       time on all GPUs.
+// Block 0 runs the control epilogue right after H1.
+// Reuse, by construction: rank q rewrites parity slot (t & 1) of r's inbox
+// (K1 pushes, H1 slot) only in step t+2, after its step t+1 polled every
+// contribution of r for step t+1, which r's blocks store only after their
+// exchange(t) completed. A contribution word of step t+1 can overwrite one of
+// step t only after r saw q's H1(t+1), which q publishes after its exchange(t).
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// {payload, epoch} words of one contribution: 1 for fp32, 2 for fp64
+template <typename T> struct LL;
+template <> struct LL<float> {
+  static constexpr int W = 1;
+  __device__ static void put(unsigned long long* p, float v, uint32_t ep) {
+    st_relaxed_sys_u64(p, ((unsigned long long)ep << 32) | __float_as_uint(v));
+  }
+  __device__ static bool get(const unsigned long long* p, uint32_t ep, float& v) {
+    const unsigned long long w = ld_relaxed_sys(p);
+    v = __uint_as_float((uint32_t)w);
+    return (uint32_t)(w >> 32) == ep;
+  }
+};
+template <> struct LL<double> {
+  static constexpr int W = 2;
+  __device__ static void put(unsigned long long* p, double v, uint32_t ep) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    st_relaxed_sys_u64(p, ((unsigned long long)ep << 32) | (b & 0xffffffffull));
+    st_relaxed_sys_u64(p + 1, ((unsigned long long)ep << 32) | (b >> 32));
+  }
+  __device__ static bool get(const unsigned long long* p, uint32_t ep, double& v) {
+    const unsigned long long lo = ld_relaxed_sys(p), hi = ld_relaxed_sys(p + 1);
+    v = __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
+    return (uint32_t)(lo >> 32) == ep && (uint32_t)(hi >> 32) == ep;
+  }
+};
+
+constexpr int kXUnroll = 4;   // union entries per thread in flight
+constexpr int kXPeers = 4;    // peer words per entry polled together
+
+template <typename T>
+// 3 blocks per SM by registers: the 2-per-SM grid + block 0 is always resident
+__global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, RunConst rc) {
+  using P = typename Pair<T>::P;
+  constexpr int CH = chunk_of<T>();
+  constexpr int TILE = tile_of<T>();
+  constexpr int W = LL<T>::W;
+  __shared__ int64_t s_red[kWarps];
+  __shared__ double s_dred[kWarps];
+  __shared__ int s_off[kThreads + 1];
+  __shared__ int s_wtot[kWarps];
+  __shared__ int64_t s_poff[EXD_MAX_WORKERS + 1];   // union offset of partition p
+  __shared__ int32_t s_prank[EXD_MAX_WORKERS];      // rank holding partition p
+  __shared__ int32_t s_ft[EXD_MAX_WORKERS];         // first tile of partition p
+  __shared__ int32_t s_tcum[EXD_MAX_WORKERS + 1];   // tiles of partitions < p
+  __shared__ int64_t s_fc[EXD_MAX_WORKERS];         // first chunk of partition p
+  __shared__ int32_t s_bcum[EXD_MAX_WORKERS + 1];   // work blocks of partitions < p
+  __shared__ bool s_ok;
+  const SelectArgs& sa = a.s;
+  Ctrl* ctrl = sa.ctrl;
+  const int n = rc.n, me = a.me;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x - 1, r = (int)blockIdx.x - 1;
+  const int par = (int)(sa.t & 1);
+  const PeerFlags* inbox = a.inbox + par * n;  // this step's H1 slots
+  // (no griddepcontrol.launch_dependents: a dependent grid must not take SM
+  // slots before every block of this one is resident)
+
+  if (r < 0) {
+    // ---- block 0: totals, H1, control epilogue
+    __shared__ EpiShared esh;
+    __shared__ int64_t s_k;
+    __shared__ double s_n2;
+    const Plan& plan = ctrl->plan[par];
+    const int64_t st = plan.st, end = plan.end;
+    const int ft = (int)(st / TILE), lt = (int)((end - 1) / TILE);
+    epi_load(esh, ctrl);  // the stream kernel never writes the control block
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) PROBE(0);
+    for (int i = tid; i < rc.n_b; i += kThreads) sa.blk_next[i] = 0;
+    const int nt = (int)((rc.n_g + TILE - 1) / TILE);
+    double pn = 0.0;
+    int64_t pk = 0;
+    for (int i = tid; i < nt; i += kSumUnroll * kThreads) {
+      double v[kSumUnroll];
+      int c[kSumUnroll];
+#pragma unroll
+      for (int k = 0; k < kSumUnroll; ++k) {
+        const int ik = i + k * kThreads;
+        v[k] = ik < nt ? __ldcg(&sa.tile_norm[ik]) : 0.0;
+        c[k] = (ik < nt && ik >= ft && ik <= lt) ? __ldcg(&sa.tile_count[ik]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < kSumUnroll; ++k) {
+        pn += v[k];
+        pk += c[k];
+      }
+    }
+    pn = warp_sum(pn);
+    pk = warp_sum(pk);
+    if (lane == 0) {
+      s_dred[warp] = pn;
+      s_red[warp] = pk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double n2 = 0.0;
+      int64_t kt = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        n2 += s_dred[w];
+        kt += s_red[w];
+      }
+      s_k = kt;
+      s_n2 = n2;
+      sa.cnt_out->k = kt;
+      sa.cnt_out->norm2 = n2;
+      sa.cnt_out->capped = 0;
+    }
+    __syncthreads();
+    if (tid < n) {  // H1: one system fence orders K1's pushes and the counts before the epoch
+      PeerFlags* slot = a.peer_slot[tid] + par * n;
+      st_relaxed_sys_i64(&slot->k, s_k);
+      st_relaxed_sys_f64(&slot->norm2, s_n2);
+      st_relaxed_sys_i64(&slot->capped, 0);
+      st_relaxed_sys_i64(&slot->st, st);
+      st_relaxed_sys_i64(&slot->end, end);
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      st_relaxed_sys(&slot->count_epoch, a.epoch);
+    }
+    if (tid == 0) {
+      PROBE(1);
+      s_ok = poll_inbox_open_gate(inbox, n, false, a.epoch, &a.gate[0], a.err);
+      PROBE(2);
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    for (int q = tid; q < n; q += kThreads) {
+      const int64_t k = __ldcg(&inbox[q].k);
+      const double n2 = __ldcg(&inbox[q].norm2);
+      esh.k_rank[q] = k;
+      esh.norm2[q] = n2;
+      esh.capped[q] = 0;
+      a.counts_all[q].k = k;
+      a.counts_all[q].norm2 = n2;
+      a.counts_all[q].capped = 0;
+    }
+    __syncthreads();
+    epi_run_store(esh, ctrl, rc, a.rec);
+    if (tid == 0) PROBE(4);
+    return;
+  }
+
+  // ---- work blocks
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // own K1 complete
+  if (tid == 0) s_ok = wait_gate(&a.gate[0], a.epoch, a.err);  // every rank's H1
+  __syncthreads();
+  if (!s_ok) return;
+  if (r == 0) PROBE(8);
+  if (tid == 0) {
+    // partition p is held by rank (p - t) mod n (allocator.cpp:92-99); its
+    // range came with the holder's H1
+    const int tm = (int)mod_floor(sa.t, n);
+    int64_t off = 0;
+    int32_t tc = 0;
+    for (int p = 0; p < n; ++p) {
+      const int rk = p - tm < 0 ? p - tm + n : p - tm;
+      const int64_t pst = __ldcg(&inbox[rk].st), pend = __ldcg(&inbox[rk].end);
+      s_prank[p] = rk;
+      s_poff[p] = off;
+      s_ft[p] = (int32_t)(pst / TILE);
+      s_fc[p] = pst / CH;
+      s_tcum[p] = tc;
+      off += __ldcg(&inbox[rk].k);
+      tc += pend > pst ? (int32_t)((pend - 1) / TILE - pst / TILE + 1) : 0;
+    }
+    s_poff[n] = off;
+    s_tcum[n] = tc;
+    // work blocks per partition, by tiles, at least one each (G >= n)
+    for (int p = 0; p <= n; ++p)
+      s_bcum[p] = p + (int32_t)(((int64_t)(G - n) * s_tcum[p]) / (tc > 0 ? tc : 1));
+  }
+  __syncthreads();
+
+  // ---- this block's segment of one partition: contributions out, sums in
+  {
+    T* __restrict__ e = static_cast<T*>(sa.e);
+    T* __restrict__ x = static_cast<T*>(sa.x);
+    T* __restrict__ gsum = static_cast<T*>(a.sum);
+    const uint32_t ep = (uint32_t)a.epoch;
+    int p = 0;
+    while (p + 1 < n && s_bcum[p + 1] <= r) ++p;
+    const int rl = r - s_bcum[p], nbl = s_bcum[p + 1] - s_bcum[p];
+    const int ntp = s_tcum[p + 1] - s_tcum[p];
+    const int rk = s_prank[p];
+    const bool own = rk == me;
+    const int ftp = s_ft[p];
+    const int32_t* tcnt = own ? sa.tile_count : a.tile_in[par][rk];
+    const int32_t* ccnt = own ? sa.chunk_count : a.chunk_in[par][rk];
+    const int32_t* sidx = a.stage_in[par][rk];
+    const P* sp = static_cast<const P*>(sa.stage);
+    const int t0 = ftp + (int)(((int64_t)ntp * rl) / nbl);
+    const int t1 = ftp + (int)(((int64_t)ntp * (rl + 1)) / nbl);
+    const int nch = (t1 - t0) * kWarps;
+    int cnt = tid < nch ? __ldcg(&ccnt[t0 * kWarps + tid]) : 0;  // issued before the prefix
+    int64_t running = cta_sum_counts(tcnt, ftp, t0, s_red);  // partition-local index of t0's first entry
+    PROBE_MAX(41);
+    for (int cb = 0; cb < nch; cb += kThreads) {
+      const int nb = nch - cb < kThreads ? nch - cb : kThreads;
+      if (cb) cnt = tid < nb ? __ldcg(&ccnt[t0 * kWarps + cb + tid]) : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wtot[warp] = incl;
+      __syncthreads();
+      int wpre = 0, btot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        wpre += w < warp ? s_wtot[w] : 0;
+        btot += s_wtot[w];
+      }
+      s_off[tid] = wpre + incl - cnt;
+      __syncthreads();
+      const int64_t cbase = (int64_t)(t0 * kWarps + cb) - s_fc[p];
+      for (int i0 = tid; i0 < btot; i0 += kXUnroll * kThreads) {
+        int32_t jj[kXUnroll];
+        T vv[kXUnroll];
+#pragma unroll
+        for (int q = 0; q < kXUnroll; ++q) {
+          const int i = i0 + q * kThreads;
+          jj[q] = 0;
+          vv[q] = T(0);
+          if (i < btot) {
+            int lo = 0, hi = nb;  // last chunk k with s_off[k] <= i
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (s_off[mid] <= i) lo = mid; else hi = mid;
+            }
+            const int64_t src = (cbase + lo) * CH + (i - s_off[lo]);
+            if (own) {
+              const P pr = __ldcg(&sp[src]);
+              jj[q] = (int32_t)Pair<T>::idx(pr);
+              vv[q] = Pair<T>::val(pr);
+            } else {
+              jj[q] = __ldcg(&sidx[src]);
+            }
+          }
+        }
+#ifdef EXD_PROBE
+        if (jj[0] == 0x7fffffff) g_probe[63] = 1;  // force the loads before the stamp
+        PROBE_MAX(42);
+#endif
+        T xv[kXUnroll];
+#pragma unroll
+        for (int q = 0; q < kXUnroll; ++q) {
+          if (i0 + q * kThreads >= btot) continue;
+          if (!own) vv[q] = e[jj[q]];
+          xv[q] = x[jj[q]];
+        }
+        // own contribution out (every peer's inbox), union entry, residual clear
+#pragma unroll
+        for (int q = 0; q < kXUnroll; ++q) {
+          const int i = i0 + q * kThreads;
+          if (i >= btot) continue;
+          const int64_t lp = running + i, pos = s_poff[p] + lp;
+          for (int rr = 0; rr < n; ++rr)
+            if (rr != me)
+              LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[rr]) + pos * W, vv[q], ep);
+          a.idx_global[pos] = jj[q];
+          if (own) {
+            sa.idx[lp] = jj[q];
+            static_cast<T*>(sa.val)[lp] = vv[q];
+          } else {
+            e[jj[q]] = T(0);  // own partition was cleared by the stream kernel
+          }
+        }
+#ifdef EXD_PROBE
+        PROBE_MAX(43);
+#endif
+        // the peers' contributions for the same positions; rank-order sum
+        T sv[kXUnroll];
+        for (int r0 = 0; r0 < n; r0 += kXPeers) {
+          T pv[kXUnroll][kXPeers];
+          bool ok[kXUnroll][kXPeers];
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q)
+#pragma unroll
+            for (int b = 0; b < kXPeers; ++b) {
+              const int rr = r0 + b;
+              pv[q][b] = vv[q];
+              ok[q][b] = true;
+              if (rr < n && rr != me && i0 + q * kThreads < btot)
+                ok[q][b] = LL<T>::get(static_cast<const unsigned long long*>(a.contrib_in[rr]) +
+                                          (s_poff[p] + running + i0 + q * kThreads) * W, ep, pv[q][b]);
+            }
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q)
+#pragma unroll
+            for (int b = 0; b < kXPeers; ++b) {
+              if (ok[q][b]) continue;
+              const unsigned long long* w = static_cast<const unsigned long long*>(
+                  a.contrib_in[r0 + b]) + (s_poff[p] + running + i0 + q * kThreads) * W;
+              const unsigned long long tw = gtime_ns();
+              unsigned spins = 0;
+              while (!LL<T>::get(w, ep, pv[q][b])) {
+                if ((++spins & 255u) == 0 &&
+                    (gtime_ns() - tw > 20000000000ull || *(volatile unsigned int*)a.err)) {
+                  atomicExch(a.err, 1u);  // a dead peer: the step reports EXD_ENCCL
+                  break;
+                }
+                __nanosleep(20);
+              }
+            }
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q)
+#pragma unroll
+            for (int b = 0; b < kXPeers; ++b)
+              if (r0 + b < n) sv[q] = r0 + b == 0 ? pv[q][b] : sv[q] + pv[q][b];
+        }
+#pragma unroll
+        for (int q = 0; q < kXUnroll; ++q) {
+          const int i = i0 + q * kThreads;
+          if (i >= btot) continue;
+          gsum[s_poff[p] + running + i] = sv[q];
+          x[jj[q]] = apply_update<T>(xv[q], sv[q], n);
+        }
+      }
+      running += btot;
+      __syncthreads();
+    }
+  }
+  if (r == 0) PROBE(9);
+  PROBE_MAX(44);
 }
 
 template <typename T> struct Bits;
@@ -1627,6 +2035,21 @@ cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s) {
   const int blocks = p2p_blocks() + 1;
   if (rc.dtype == EXD_F64) return launch_pdl(p2p_sync_kernel<double>, blocks, s, a, rc);
   return launch_pdl(p2p_sync_kernel<float>, blocks, s, a, rc);
+}
+
+cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s) {
+  // every block must be resident (in-kernel arrive counter): 2 per SM + block 0
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p2p_blocks() + 1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (rc.dtype == EXD_F64) return cudaLaunchKernelEx(&cfg, exchange_kernel<double>, a, rc);
+  return cudaLaunchKernelEx(&cfg, exchange_kernel<float>, a, rc);
 }
 
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {

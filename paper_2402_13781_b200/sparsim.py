@@ -221,7 +221,7 @@ class EngineOptions:
     record_loss: bool = True
     dtype: str = "f32"
     profile_kernels: bool = False
-    sync: str = "auto"          # one rank per GPU: "auto" | "nccl" | "p2p"
+    sync: str = "auto"          # one rank per GPU: "auto" | "nccl" | "p2p" | "p2p-pull"
 
     def to_c(self):
         o = A.exd_options()
@@ -234,7 +234,8 @@ class EngineOptions:
         o.record_loss = int(self.record_loss)
         o.dtype = _dtype_code(self.dtype)
         o.profile_kernels = int(self.profile_kernels)
-        o.sync_mode = {"auto": A.EXD_SYNC_AUTO, "nccl": A.EXD_SYNC_NCCL, "p2p": A.EXD_SYNC_P2P}[self.sync]
+        o.sync_mode = {"auto": A.EXD_SYNC_AUTO, "nccl": A.EXD_SYNC_NCCL, "p2p": A.EXD_SYNC_P2P,
+                       "p2p-pull": A.EXD_SYNC_P2P_PULL}[self.sync]
         return o
 
 
@@ -404,8 +405,9 @@ class Engine:
         return self.L.exd_engine_iteration(self.h)
 
     def sync_mode(self):
-        """'p2p' / 'nccl' for a rank engine, 'in-process' otherwise."""
-        return {-1: "in-process", A.EXD_SYNC_P2P: "p2p", A.EXD_SYNC_NCCL: "nccl"}[
+        """'p2p' (owner-reduce) / 'p2p-pull' / 'nccl' for a rank engine, 'in-process' otherwise."""
+        return {-1: "in-process", A.EXD_SYNC_P2P: "p2p", A.EXD_SYNC_P2P_PULL: "p2p-pull",
+                A.EXD_SYNC_NCCL: "nccl"}[
             self.L.exd_engine_sync_mode(self.h)]
 
     def stream(self, w=0):

@@ -25,9 +25,14 @@ def _run(nproc, *args, port=29577):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("sync", ["p2p", "nccl"])
+@pytest.mark.parametrize("sync", ["p2p", "p2p-pull", "nccl"])
 def test_two_ranks_bit_exact_vs_oracle(sync):
     _run(2, "--sync", sync, "--steps", "12")
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_two_ranks_owner_reduce_f64_vs_oracle():
+    _run(2, "--sync", "p2p", "--dtype", "f64", "--steps", "8", port=29581)
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
@@ -42,5 +47,6 @@ def test_replica_divergence_detected_across_gpus(sync):
 
 
 @pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
-def test_four_ranks_p2p_rank_order_sum_is_bit_exact():
-    _run(4, "--sync", "p2p", "--steps", "12", port=29580)
+@pytest.mark.parametrize("sync", ["p2p", "p2p-pull"])
+def test_four_ranks_p2p_rank_order_sum_is_bit_exact(sync):
+    _run(4, "--sync", sync, "--steps", "12", port=29580)

@@ -25,7 +25,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--d", type=float, default=0.01)
     ap.add_argument("--skew", type=int, default=1)
-    ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p"])
+    ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p", "p2p-pull"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cap", type=float, default=None, help="max_density_cap")
     ap.add_argument("--inject", type=int, default=0,
                     help="perturb x on rank 1 after step 2; the next step must raise EngineError "
@@ -48,19 +49,21 @@ def main():
               max_density_cap=args.cap)
     ids = [S.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
-    eng = S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype="f32", sync=args.sync),
+    eng = S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype=args.dtype, sync=args.sync),
                         rank, local, ids[0])
     segs = O.skew_segments(args.n_g) if args.skew else None
     src = S.SyntheticStream(S.StreamSpec(n_g=args.n_g, segments=segs, seed=5))
-    buf = torch.empty(args.n_g, device=f"cuda:{local}")
-    orc = O.OracleEngine(O.make_config(**kw), np.float32) if rank == 0 else None
-    tmp = torch.empty(args.n_g, device=f"cuda:{local}")
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    buf = torch.empty(args.n_g, dtype=tdt, device=f"cuda:{local}")
+    orc = O.OracleEngine(O.make_config(**kw), np.float32 if args.dtype == "f32" else np.float64) \
+        if rank == 0 else None
+    tmp = torch.empty(args.n_g, dtype=tdt, device=f"cuda:{local}")
     ok = True
     if args.inject:
         msg = ""
         try:
             for t in range(5):
-                src.gradient(t, rank, buf, "f32", eng.stream())
+                src.gradient(t, rank, buf, args.dtype, eng.stream())
                 torch.cuda.synchronize()
                 eng.step([buf])
                 if t == 2 and rank == 1:
@@ -78,13 +81,13 @@ def main():
         dist.destroy_process_group()
         sys.exit(0 if all(f[0] for f in flags) else 1)
     for t in range(args.steps):
-        src.gradient(t, rank, buf, "f32", eng.stream())
+        src.gradient(t, rank, buf, args.dtype, eng.stream())
         torch.cuda.synchronize()
         rec = eng.step([buf])
         if rank == 0:
             host = []
             for r in range(world):
-                src.gradient(t, r, tmp, "f32", 0)
+                src.gradient(t, r, tmp, args.dtype, 0)
                 torch.cuda.synchronize()
                 host.append(tmp.cpu().numpy().copy())
             orec = orc.step(host)
@@ -131,7 +134,7 @@ def main():
             if not np.array_equal(m["sel"].astype(np.int64), orc.selection(r)):
                 print(f"[rank0] rank {r} selection differs", flush=True)
                 ok = False
-        print(f"dist_check world={world} sync={args.sync} cap={args.cap} n_g={args.n_g} steps={args.steps}: "
+        print(f"dist_check world={world} sync={args.sync} ({eng.sync_mode()}) dtype={args.dtype} cap={args.cap} n_g={args.n_g} steps={args.steps}: "
               f"{'PASS' if ok else 'FAIL'} (last k'={rec.k_prime} f_t={rec.f_t:.3f})", flush=True)
     flag = torch.tensor([1 if ok else 0])
     dist.broadcast(flag, src=0)

@@ -3,7 +3,8 @@ EXD_LIB=paper_2402_13781_b200/lib/libexdyna_probe.so torchrun --nproc-per-node 2
 """
 import argparse, ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-ap = argparse.ArgumentParser(); ap.add_argument("--sync", default="p2p"); ap.add_argument("--flush", type=int, default=0)
+ap = argparse.ArgumentParser(); ap.add_argument("--sync", default="p2p")  # p2p | p2p-pull | nccl
+ap.add_argument("--flush", type=int, default=0)
 a = ap.parse_args()
 import torch, torch.distributed as dist
 from paper_2402_13781_b200 import sparsim as S
@@ -34,7 +35,12 @@ if hasattr(L, "exd_debug_probe"):
     L.exd_debug_probe.argtypes = [C.POINTER(C.c_uint64)]
     buf = (C.c_uint64 * 64)(); L.exd_debug_probe(buf)
     t0 = buf[16]
-    names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "sync", 21: "counts_in", 22: "contrib_done", 23: "contribs_in", 24: "epi_end", 25: "b0_end"}
+    if eng.sync_mode() == "p2p":  # push-reduce exchange kernel
+        names = {16: "k1", 17: "k1_last", 0: "x_start", 1: "h1_sent", 2: "h1_in", 8: "w0_gate0",
+                 41: "max_base", 42: "max_stage_ld", 43: "max_put", 9: "w0_done", 44: "max_done",
+                 4: "epi_end"}
+    else:
+        names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "sync", 21: "counts_in", 22: "contrib_done", 23: "contribs_in", 24: "epi_end", 25: "b0_end"}
     out += "  | " + "  ".join(f"{v}={(buf[k]-t0)/1e3:.1f}" for k, v in sorted(names.items(), key=lambda kv: buf[kv[0]]) if buf[k])
 print(out, flush=True)
 dist.barrier(); dist.destroy_process_group()
