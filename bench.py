@@ -326,6 +326,8 @@ def run_ours(args):
     e2e_steps = max(3, min(args.steps, 20))
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(e2e_steps)]
+    # one untimed call first: it allocates the engine's device staging buffer
+    check(L.exd_engine_step_host(eng.h, (C.c_void_p * 1)(host[1].data_ptr()), C.byref(rec)))
     barrier()
     for k in range(e2e_steps):
         S.flush_l2(local, eng.stream())
@@ -334,6 +336,9 @@ def run_ours(args):
         check(L.exd_engine_step_host(eng.h, ptrs, C.byref(rec)))  # returns with the record on the host
         ev2[k][1].record(stream)
     barrier()
+    if os.environ.get("EXD_BENCH_VERBOSE"):
+        print(f"[rank {rank}] e2e ms: {[round(a.elapsed_time(b), 3) for a, b in ev2]}",
+              file=sys.stderr, flush=True)
     e2e_total = max_over_ranks([sum(a.elapsed_time(b) for a, b in ev2)], dist)[0]
     e2e_ms = e2e_total / e2e_steps
     clk = clocks.stop()
@@ -371,7 +376,8 @@ def run_ours(args):
     cfg_line = workload(n)
     if n > 1:
         cfg_line["sync"] = {
-            "p2p": "NVLink peer memory, owner-reduce (peer residuals read in place; no host wait)",
+            "p2p": "NVLink peer memory, push-reduce (lists pushed during the stream, "
+                   "{value, epoch} contribution words; one handshake, no host wait)",
             "p2p-pull": "NVLink peer memory, pull-reduce (lists pushed, contributions pulled)",
             "nccl": "NCCL all-gather/all-reduce + one host wait"}[eng.sync_mode()]
     line = {

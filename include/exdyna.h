@@ -90,9 +90,10 @@ enum {
   EXD_SYNC_AUTO = 0,   /* NVLink peer memory when every peer is P2P-reachable, else NCCL */
   EXD_SYNC_NCCL = 1,   /* count all-gather, host wait, padded index all-gather, all-reduce */
   EXD_SYNC_P2P = 2,    /* peer-memory kernels, no host in the loop (fails if unavailable):
-                          owner-reduce (each rank sums its own selection from the peers'
-                          residuals over NVLink), or pull-reduce under a density cap or
-                          verify_conservation */
+                          push-reduce (the stream kernel pushes its selection runs to the
+                          peers; every rank pushes its contributions as {value, epoch}
+                          words and sums them in rank order), or pull-reduce under a
+                          density cap or verify_conservation */
   EXD_SYNC_P2P_PULL = 3  /* peer-memory kernels, pull-reduce always (index lists pushed
                             first, every rank sums the whole union from the peers'
                             contribution buffers) */
@@ -245,7 +246,7 @@ void exd_engine_destroy(exd_engine* h);
 int32_t exd_engine_local_workers(const exd_engine* h);
 int32_t exd_engine_first_rank(const exd_engine* h);
 int64_t exd_engine_iteration(const exd_engine* h);
-/* collective path in use: EXD_SYNC_P2P (owner-reduce), EXD_SYNC_P2P_PULL or EXD_SYNC_NCCL
+/* collective path in use: EXD_SYNC_P2P (push-reduce), EXD_SYNC_P2P_PULL or EXD_SYNC_NCCL
    (-1: in-process workers) */
 int32_t exd_engine_sync_mode(const exd_engine* h);
 /* CUDA stream of local worker w (cudaStream_t as void*) */

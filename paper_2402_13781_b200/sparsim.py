@@ -405,7 +405,7 @@ class Engine:
         return self.L.exd_engine_iteration(self.h)
 
     def sync_mode(self):
-        """'p2p' (owner-reduce) / 'p2p-pull' / 'nccl' for a rank engine, 'in-process' otherwise."""
+        """'p2p' (push-reduce) / 'p2p-pull' / 'nccl' for a rank engine, 'in-process' otherwise."""
         return {-1: "in-process", A.EXD_SYNC_P2P: "p2p", A.EXD_SYNC_P2P_PULL: "p2p-pull",
                 A.EXD_SYNC_NCCL: "nccl"}[
             self.L.exd_engine_sync_mode(self.h)]

@@ -31,7 +31,7 @@ def test_two_ranks_bit_exact_vs_oracle(sync):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-def test_two_ranks_owner_reduce_f64_vs_oracle():
+def test_two_ranks_push_reduce_f64_vs_oracle():
     _run(2, "--sync", "p2p", "--dtype", "f64", "--steps", "8", port=29581)
 
 

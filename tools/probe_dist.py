@@ -39,6 +39,7 @@ if hasattr(L, "exd_debug_probe"):
         names = {16: "k1", 17: "k1_last", 0: "x_start", 1: "h1_sent", 2: "h1_in", 8: "w0_gate0",
                  41: "max_base", 42: "max_stage_ld", 43: "max_put", 9: "w0_done", 44: "max_done",
                  4: "epi_end"}
+        out += f"  | prev step: k1 -> max_done {(buf[50]-buf[51])/1e3:.1f} us, max_done -> this k1 {(buf[16]-buf[50])/1e3:.1f} us"
     else:
         names = {16: "k1", 17: "k1_last", 8: "k2copy0", 0: "k2epi", 3: "k2epi_end", 20: "sync", 21: "counts_in", 22: "contrib_done", 23: "contribs_in", 24: "epi_end", 25: "b0_end"}
     out += "  | " + "  ".join(f"{v}={(buf[k]-t0)/1e3:.1f}" for k, v in sorted(names.items(), key=lambda kv: buf[kv[0]]) if buf[k])
