@@ -263,8 +263,12 @@ def run_ours(args):
         extra = [int(t[0])]
     run_steps(extra[0])
     eng.reset_kernel_stats()
-    launches0 = eng.kernel_stats()["kernel_launches"]
     barrier()
+    # one untimed step right after the host barrier (the ranks leave it tens of
+    # us apart; the step's in-kernel exchange realigns them), then the device sync
+    run_steps(1)
+    torch.cuda.synchronize()
+    launches0 = eng.kernel_stats()["kernel_launches"]
 
     # ---- value: K steps, each bracketed by events on the engine's stream, L2
     # flushed before each (flush excluded). Per-kernel profiling is OFF here so

@@ -235,13 +235,15 @@ struct exd_engine {
   unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
-  //   | chunk counts[2][n] | tile counts[2][n] | contrib words[n][n_g]   ([2]: step parity)
+  //   | chunk counts[2][n] | tile counts[2][n] | contrib[2][n][n_g]   ([2]: step parity;
+  //   everything but the flags as {payload, epoch} words)
   bool xchg = false;
-  std::vector<int32_t*> push_stage[2], push_chunk[2], push_tile[2];  // [n-1] my slots in every peer's inbox
+  // ({payload, epoch} words; [2]: step parity)
+  std::vector<unsigned long long*> push_stage[2], push_chunk[2], push_tile[2];  // [n-1] my slots in every peer's inbox
   std::vector<PeerFlags*> slot_host;                   // [n] my parity-0 flag slot in every rank's inbox
-  std::vector<const int32_t*> stage_in[2], chunk_in[2], tile_in[2];  // [n] inbox slots by source
-  std::vector<void*> contrib_out;                      // [n] my contribution slot in every inbox
-  std::vector<const void*> contrib_in;                 // [n] contribution slots by source (local)
+  std::vector<const unsigned long long*> stage_in[2], chunk_in[2], tile_in[2];  // [n] inbox slots by source
+  std::vector<void*> contrib_out[2];                   // [n] my contribution slot in every inbox
+  std::vector<const void*> contrib_in[2];              // [n] contribution slots by source (local)
   unsigned long long* rep_hash = nullptr;  // [4 * (n + 1)]: own words, then all ranks' words
   int32_t* recv = nullptr;
   int64_t recv_cap = 0;
@@ -510,36 +512,54 @@ int setup_p2p(exd_engine* h) {
   // verify_conservation needs the trimmed lists and contribution buffers first
   h->xchg = h->opt.sync_mode != EXD_SYNC_P2P_PULL && h->cap == 0 && !h->opt.verify_conservation;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  // flag slots: two step parities for push-reduce
-  const size_t flags_b = al(sizeof(PeerFlags) * (size_t)n * (h->xchg ? 2 : 1));
-  size_t list_b, con_b, off_lists, off_c0, off_c1, total;
+  size_t flags_b = 0, list_b = 0, con_b = 0, off_lists = 0, off_c0 = 0, off_c1 = 0, total = 0;
   size_t stage_b = 0, chunk_b = 0, tile_b = 0, xcon_b = 0, off_st = 0, off_ch = 0, off_ti = 0, off_xc = 0;
-  if (h->xchg) {
-    // push-reduce: flags[2][n] | stage idx[2][n] | chunk counts[2][n] | tile counts[2][n]
-    //              | contribution words[n] (8 B {value, epoch} per fp32 entry, 16 B per fp64)
-    stage_b = al(4 * ((size_t)h->cap_part + 2 * (size_t)h->tile));
-    chunk_b = al(4 * (size_t)(h->tiles + 1) * kChunksPerTile);
-    tile_b = al(4 * (size_t)(h->tiles + 8));
-    xcon_b = al(2 * h->esz * (size_t)h->cfg.n_g);
-    off_st = flags_b;
-    off_ch = off_st + stage_b * 2 * n;
-    off_ti = off_ch + chunk_b * 2 * n;
-    off_xc = off_ti + tile_b * 2 * n;
-    total = off_xc + xcon_b * n;
-    list_b = con_b = off_lists = off_c0 = off_c1 = 0;
-  } else {
-    // pull-reduce: flags[n] | lists[n][cap_part] | contrib[2][n_g]
-    list_b = al(4 * (size_t)h->cap_part);
-    con_b = al(h->esz * (size_t)h->cfg.n_g);
-    off_lists = flags_b;
-    off_c0 = off_lists + list_b * (size_t)n;
-    off_c1 = off_c0 + con_b;
-    total = off_c1 + con_b;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (h->xchg) {
+      // push-reduce: flags[2][n] | stage[2][n] | chunk counts[2][n] | tile counts[2][n]
+      //              | contributions[2][n]; words: 8 B per index / count / fp32 value, 16 B per fp64
+      flags_b = al(sizeof(PeerFlags) * (size_t)n * 2);
+      stage_b = al(8 * ((size_t)h->cap_part + 2 * (size_t)h->tile));
+      chunk_b = al(8 * (size_t)(h->tiles + 1) * kChunksPerTile);
+      tile_b = al(8 * (size_t)(h->tiles + 8));
+      xcon_b = al(2 * h->esz * (size_t)h->cfg.n_g);
+      off_st = flags_b;
+      off_ch = off_st + stage_b * 2 * n;
+      off_ti = off_ch + chunk_b * 2 * n;
+      off_xc = off_ti + tile_b * 2 * n;
+      total = off_xc + xcon_b * 2 * n;
+    } else {
+      // pull-reduce: flags[n] | lists[n][cap_part] | contrib[2][n_g]
+      flags_b = al(sizeof(PeerFlags) * (size_t)n);
+      list_b = al(4 * (size_t)h->cap_part);
+      con_b = al(h->esz * (size_t)h->cfg.n_g);
+      off_lists = flags_b;
+      off_c0 = off_lists + list_b * (size_t)n;
+      off_c1 = off_c0 + con_b;
+      total = off_c1 + con_b;
+    }
+    // every rank must take the same path: agree on whether the region fits
+    int ok = cudaMalloc(&h->region, total) == cudaSuccess ? 1 : 0;
+    if (!ok) {
+      cudaGetLastError();
+      h->region = nullptr;
+    }
+    int* d_ok2 = nullptr;
+    CU(cudaMalloc((void**)&d_ok2, sizeof(int)));
+    CU(cudaMemcpy(d_ok2, &ok, sizeof(int), cudaMemcpyHostToDevice));
+    NC(nccl().AllReduce(d_ok2, d_ok2, 1, ncclInt32, ncclMin, h->comm, h->stream));
+    CU(cudaMemcpyAsync(&ok, d_ok2, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    cudaFree(d_ok2);
+    if (ok) break;
+    if (h->region) cudaFree(h->region);
+    h->region = nullptr;
+    if (!h->xchg) return set_err(EXD_ECUDA, "peer-memory inbox does not fit in device memory");
+    h->xchg = false;  // the push-reduce inbox does not fit (huge n_g): pull-reduce
   }
-  CU(cudaMalloc(&h->region, total));
   CU(cudaMemset(h->region, 0, flags_b));
-  // contribution words start with epoch 0 (never a live epoch)
-  if (h->xchg) CU(cudaMemset(static_cast<char*>(h->region) + off_xc, 0, xcon_b * n));
+  // words start with epoch 0 (never a live epoch)
+  if (h->xchg) CU(cudaMemset(static_cast<char*>(h->region) + off_st, 0, total - off_st));
   h->inbox = static_cast<PeerFlags*>(h->region);
   Worker& wk = h->w[0];
   cudaIpcMemHandle_t mine;
@@ -569,8 +589,6 @@ int setup_p2p(exd_engine* h) {
   }
   if (h->xchg) {
     char* own = static_cast<char*>(h->region);
-    h->contrib_out.assign(n, nullptr);
-    h->contrib_in.assign(n, nullptr);
     h->slot_host.assign(n, nullptr);
     for (int par = 0; par < 2; ++par) {
       h->stage_in[par].assign(n, nullptr);
@@ -580,19 +598,22 @@ int setup_p2p(exd_engine* h) {
         if (r == me) continue;
         // my slots in rank r's inbox, and rank r's slots in mine
         const size_t sm = (size_t)(par * n + me), sr = (size_t)(par * n + r);
-        h->push_stage[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_st + stage_b * sm));
-        h->push_chunk[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_ch + chunk_b * sm));
-        h->push_tile[par].push_back(reinterpret_cast<int32_t*>(base[r] + off_ti + tile_b * sm));
-        h->stage_in[par][r] = reinterpret_cast<const int32_t*>(own + off_st + stage_b * sr);
-        h->chunk_in[par][r] = reinterpret_cast<const int32_t*>(own + off_ch + chunk_b * sr);
-        h->tile_in[par][r] = reinterpret_cast<const int32_t*>(own + off_ti + tile_b * sr);
+        using W = unsigned long long;
+        h->push_stage[par].push_back(reinterpret_cast<W*>(base[r] + off_st + stage_b * sm));
+        h->push_chunk[par].push_back(reinterpret_cast<W*>(base[r] + off_ch + chunk_b * sm));
+        h->push_tile[par].push_back(reinterpret_cast<W*>(base[r] + off_ti + tile_b * sm));
+        h->stage_in[par][r] = reinterpret_cast<const W*>(own + off_st + stage_b * sr);
+        h->chunk_in[par][r] = reinterpret_cast<const W*>(own + off_ch + chunk_b * sr);
+        h->tile_in[par][r] = reinterpret_cast<const W*>(own + off_ti + tile_b * sr);
+      }
+      h->contrib_out[par].assign(n, nullptr);
+      h->contrib_in[par].assign(n, nullptr);
+      for (int r = 0; r < n; ++r) {
+        h->contrib_out[par][r] = base[r] + off_xc + xcon_b * (size_t)(par * n + me);
+        h->contrib_in[par][r] = own + off_xc + xcon_b * (size_t)(par * n + r);
       }
     }
-    for (int r = 0; r < n; ++r) {
-      h->contrib_out[r] = base[r] + off_xc + xcon_b * me;
-      h->contrib_in[r] = own + off_xc + xcon_b * r;
-      h->slot_host[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
-    }
+    for (int r = 0; r < n; ++r) h->slot_host[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
   }
   std::vector<PeerFlags*> slot(n);
   std::vector<const int32_t*> lists(n);
@@ -708,8 +729,10 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
       o.chunk_in[par][r] = h->chunk_in[par][r];
       o.tile_in[par][r] = h->tile_in[par][r];
     }
-    o.contrib_out[r] = h->contrib_out[r];
-    o.contrib_in[r] = h->contrib_in[r];
+    for (int par = 0; par < 2; ++par) {
+      o.contrib_out[par][r] = h->contrib_out[par][r];
+      o.contrib_in[par][r] = h->contrib_in[par][r];
+    }
   }
   o.idx_global = wk.idx_global;
   o.sum = h->sum;

@@ -103,9 +103,10 @@ struct SelectArgs {
   int32_t npush;
   // P2P push-reduce: the stream kernel's pushes into every peer's inbox (by
   // value: kernel parameters are constant-bank reads, no pointer round trip)
-  int32_t* push_stage[EXD_MAX_WORKERS - 1];  // [k1_npush] my staged-index slot
-  int32_t* push_chunk[EXD_MAX_WORKERS - 1];  // [k1_npush] my per-chunk count slot
-  int32_t* push_tile[EXD_MAX_WORKERS - 1];   // [k1_npush] my per-tile count slot
+  // ({payload, epoch} words, this step's parity)
+  unsigned long long* push_stage[EXD_MAX_WORKERS - 1];  // [k1_npush] my staged-index slot
+  unsigned long long* push_chunk[EXD_MAX_WORKERS - 1];  // [k1_npush] my per-chunk count slot
+  unsigned long long* push_tile[EXD_MAX_WORKERS - 1];   // [k1_npush] my per-tile count slot
   int32_t k1_npush;             // 0: no pushes
 };
 
@@ -179,11 +180,12 @@ struct ExchangeArgs {
   // pointer tables by value (constant bank)
   PeerFlags* peer_slot[EXD_MAX_WORKERS];        // my parity-0 flag slot in every rank's inbox
   // [step parity][source rank]: pushed staged-index runs / per-chunk / per-tile counts (local)
-  const int32_t* stage_in[2][EXD_MAX_WORKERS];
-  const int32_t* chunk_in[2][EXD_MAX_WORKERS];
-  const int32_t* tile_in[2][EXD_MAX_WORKERS];
-  void* contrib_out[EXD_MAX_WORKERS];           // my {value, epoch} slot in every rank's inbox
-  const void* contrib_in[EXD_MAX_WORKERS];      // {value, epoch} slots by source rank (local)
+  // ({payload, epoch} words)
+  const unsigned long long* stage_in[2][EXD_MAX_WORKERS];
+  const unsigned long long* chunk_in[2][EXD_MAX_WORKERS];
+  const unsigned long long* tile_in[2][EXD_MAX_WORKERS];
+  void* contrib_out[2][EXD_MAX_WORKERS];        // [parity] my {value, epoch} slot in every inbox
+  const void* contrib_in[2][EXD_MAX_WORKERS];   // [parity] {value, epoch} slots by source (local)
   int32_t* idx_global;               // [k'] union, partition order
   void* sum;                         // [k'] aggregated values (T)
   CountRec* counts_all;              // [n] local copy of the gathered counts

@@ -313,6 +313,21 @@ __device__ __forceinline__ uint32_t block_of(uint32_t j, const RunConst& rc) {
   return b < (uint32_t)(rc.n_b - 1) ? b : (uint32_t)(rc.n_b - 1);
 }
 
+// {payload, epoch} words (the low-latency protocol of the push-reduce sync):
+// each aligned 8-byte word is single-copy atomic, so it is its own flag
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_v2u64(unsigned long long* p, unsigned long long a,
+                                                     unsigned long long b) {
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // PUSH (one rank per GPU, push-reduce sync): the staged indices and the
 // per-chunk / per-tile counts of the partition also go to every peer's inbox.
 template <typename T, int MODE, bool UNIT, bool PUSH>
@@ -485,11 +500,14 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     }
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
     if (PUSH && running) {
-      // the run sbase + [0, running) in every peer's staging slot: 128 B stores
+      // the run sbase + [0, running) in every peer's staging slot as
+      // {index, epoch} words: 256 B coalesced stores, each word its own flag
       __syncwarp();
+      const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
       for (int q = 0; q < a.k1_npush; ++q) {
-        int32_t* dst = a.push_stage[q] + sbase;
-        for (int i = lane; i < running; i += 32) dst[i] = s_run[warp * CH + i];
+        unsigned long long* dst = a.push_stage[q] + sbase;
+        for (int i = lane; i < running; i += 32)
+          st_relaxed_sys_u64(dst + i, eph | (uint32_t)s_run[warp * CH + i]);
       }
     }
   }
@@ -519,15 +537,13 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
       for (int w = 0; w < kWarps; ++w) sc += s_cnt[w];
       a.tile_count[tile] = sc;
       if (push_tile) {
-        // the tile's kWarps chunk counts as two 16 B stores, then its count
-        static_assert(kWarps == 8, "two int4 per tile");
-        const int4 c0 = make_int4(s_cnt[0], s_cnt[1], s_cnt[2], s_cnt[3]);
-        const int4 c1 = make_int4(s_cnt[4], s_cnt[5], s_cnt[6], s_cnt[7]);
+        // the tile's kWarps chunk counts and its count as {count, epoch} words
+        const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
         for (int q = 0; q < a.k1_npush; ++q) {
-          int4* d = reinterpret_cast<int4*>(a.push_chunk[q] + tile * kWarps);
-          d[0] = c0;
-          d[1] = c1;
-          a.push_tile[q][tile] = sc;
+          unsigned long long* d = a.push_chunk[q] + tile * kWarps;
+#pragma unroll
+          for (int w = 0; w < kWarps; w += 2) st_relaxed_sys_v2u64(d + w, eph | (uint32_t)s_cnt[w], eph | (uint32_t)s_cnt[w + 1]);
+          st_relaxed_sys_u64(a.push_tile[q] + tile, eph | (uint32_t)sc);
         }
       }
     }
@@ -676,9 +692,10 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's counts and runs
   const int t0 = ft + (int)(((int64_t)ntp * r) / G);
   const int t1 = ft + (int)(((int64_t)ntp * (r + 1)) / G);
-  const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
   const int nch = (t1 - t0) * kWarps;
+  // the chunk counts do not depend on the base: load them in the same round trip
   int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
+  const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
   if (r == 0) PROBE(9);
   if (r == G - 1) PROBE(10);
   CPROBE(1, r);
@@ -1163,37 +1180,36 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
 }
 
 // ---- f1, push-reduce: the whole sync in the kernel after the stream ---------
-// One rank per GPU, no density cap. Replaces finish + p2p_sync with ONE kernel,
-// ONE cross-GPU handshake, and only posted NVLink stores (no remote reads):
+// One rank per GPU, no density cap. Replaces finish + p2p_sync with ONE kernel.
+// Everything crosses NVLink as posted stores of {payload, epoch} words (the
+// low-latency protocol: an aligned 8-byte word is single-copy atomic, so the
+// word is its own flag): no remote reads, no fences and no handshake on the
+// critical path.
 //   K1  (stream_kernel<..., PUSH>) besides staging its (index, value) pairs
-//       locally, copies each warp's run of staged indices and the per-chunk /
-//       per-tile counts of its partition into its slots of every peer's inbox
-//       (slots double-buffered by step parity).
-//   H1  block 0 totals this rank's counts once K1 is complete and publishes
-//       {k_i, ||e||^2, partition range} + epoch into every rank's inbox (one
-//       system fence also covers K1's pushes).
-//   A+B every work block owns one contiguous segment of ONE partition's union
+//       locally, stores each warp's run of staged indices and its tile's chunk
+//       and tile counts into its slots of every peer's inbox as words tagged
+//       with the step.
+//   A+B every work block owns a contiguous tile range of ONE partition (the
+//       partition table is the replicated plan; allocator.cpp:92-99). Its union
 //       positions (collectives.cpp:47-55: the union is the concatenation of the
-//       ascending lists in partition order), located from the holder's chunk /
-//       tile counts exactly as the finish kernel does. Per entry, one thread:
-//       gathers its own contribution acc[j] (engine.cpp:310-317), stores it
-//       into every peer's inbox as a 64-bit {value, epoch} word (the low-latency
-//       protocol: the word is its own flag, so no fence and no second
-//       handshake), clears e[j] (selector.cpp:63-65), then polls the peers'
-//       words for the same position, sums the n contributions in rank order
+//       ascending lists in partition order) come from the tile counts of every
+//       tile before its range and from its chunk counts, polled as words. Per
+//       entry, one thread: takes the index from the holder's pushed run (own
+//       staged pairs for its own partition), gathers its own contribution
+//       acc[j] (engine.cpp:310-317), stores it as a word into every peer's
+//       inbox, clears e[j] (selector.cpp:63-65), then polls the peers' words
+//       for the same position, sums the n contributions in rank order
 //       (all_reduce_sum, collectives.cpp:62-68: bit-identical for every n) and
-//       applies x -= g/n (engine.cpp:215). Every rank runs the same position
-//       split, so a position's n contributions are produced at about the same
-//       time on all GPUs.
-// Block 0 runs the control epilogue right after H1.
-// Reuse, by construction: rank q rewrites parity slot (t & 1) of r's inbox
-// (K1 pushes, H1 slot) only in step t+2, after its step t+1 polled every
-// contribution of r for step t+1, which r's blocks store only after their
-// exchange(t) completed. A contribution word of step t+1 can overwrite one of
-// step t only after r saw q's H1(t+1), which q publishes after its exchange(t).
-__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
+//       applies x -= g/n (engine.cpp:215).
+//   block 0 totals this rank's {k_i, ||e||^2}, exchanges them with a flag (off
+//       the critical path: only the control epilogue needs every rank's
+//       counts) and runs the epilogue.
+// Reuse, by construction: every inbox slot (pushed runs and counts, flags,
+// contribution words) is double-buffered by step parity. Rank q rewrites
+// parity slot (t & 1) of r's inbox only in step t+2, after its step t+1 polled
+// every contribution word of r for step t+1, which r's blocks store only
+// after r's kernels of step t completed. A stale word carries an older epoch
+// and is polled again.
 
 // {payload, epoch} words of one contribution: 1 for fp32, 2 for fp64
 template <typename T> struct LL;
@@ -1203,7 +1219,7 @@ template <> struct LL<float> {
     st_relaxed_sys_u64(p, ((unsigned long long)ep << 32) | __float_as_uint(v));
   }
   __device__ static bool get(const unsigned long long* p, uint32_t ep, float& v) {
-    const unsigned long long w = ld_relaxed_sys(p);
+    const unsigned long long w = ld_relaxed_sys_u64(p);
     v = __uint_as_float((uint32_t)w);
     return (uint32_t)(w >> 32) == ep;
   }
@@ -1212,15 +1228,32 @@ template <> struct LL<double> {
   static constexpr int W = 2;
   __device__ static void put(unsigned long long* p, double v, uint32_t ep) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    st_relaxed_sys_u64(p, ((unsigned long long)ep << 32) | (b & 0xffffffffull));
-    st_relaxed_sys_u64(p + 1, ((unsigned long long)ep << 32) | (b >> 32));
+    st_relaxed_sys_v2u64(p, ((unsigned long long)ep << 32) | (b & 0xffffffffull),
+                         ((unsigned long long)ep << 32) | (b >> 32));
   }
   __device__ static bool get(const unsigned long long* p, uint32_t ep, double& v) {
-    const unsigned long long lo = ld_relaxed_sys(p), hi = ld_relaxed_sys(p + 1);
+    const unsigned long long lo = ld_relaxed_sys_u64(p), hi = ld_relaxed_sys_u64(p + 1);
     v = __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
     return (uint32_t)(lo >> 32) == ep && (uint32_t)(hi >> 32) == ep;
   }
 };
+
+// Poll one {count, epoch} word until it carries `ep`; gives up after 20 s
+// (sets *err, returns 0) so a dead peer cannot hang the GPU.
+__device__ __noinline__ uint32_t poll_word(const unsigned long long* p, uint32_t ep, unsigned int* err) {
+  const unsigned long long t0 = gtime_ns();
+  unsigned spins = 0;
+  unsigned long long w;
+  while ((uint32_t)((w = ld_relaxed_sys_u64(p)) >> 32) != ep) {
+    if ((++spins & 255u) == 0 &&
+        (gtime_ns() - t0 > 20000000000ull || *(volatile unsigned int*)err)) {
+      atomicExch(err, 1u);
+      return 0;
+    }
+    __nanosleep(20);
+  }
+  return (uint32_t)w;
+}
 
 constexpr int kXUnroll = 4;   // union entries per thread in flight
 constexpr int kXPeers = 4;    // peer words per entry polled together
@@ -1236,7 +1269,6 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   __shared__ double s_dred[kWarps];
   __shared__ int s_off[kThreads + 1];
   __shared__ int s_wtot[kWarps];
-  __shared__ int64_t s_poff[EXD_MAX_WORKERS + 1];   // union offset of partition p
   __shared__ int32_t s_prank[EXD_MAX_WORKERS];      // rank holding partition p
   __shared__ int32_t s_ft[EXD_MAX_WORKERS];         // first tile of partition p
   __shared__ int32_t s_tcum[EXD_MAX_WORKERS + 1];   // tiles of partitions < p
@@ -1249,16 +1281,15 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x - 1, r = (int)blockIdx.x - 1;
   const int par = (int)(sa.t & 1);
-  const PeerFlags* inbox = a.inbox + par * n;  // this step's H1 slots
-  // (no griddepcontrol.launch_dependents: a dependent grid must not take SM
-  // slots before every block of this one is resident)
+  const uint32_t ep = (uint32_t)a.epoch;
+  const Plan& plan = ctrl->plan[par];  // the epilogue writes only the other slot
 
   if (r < 0) {
-    // ---- block 0: totals, H1, control epilogue
+    // ---- block 0: totals, count exchange, control epilogue
     __shared__ EpiShared esh;
     __shared__ int64_t s_k;
     __shared__ double s_n2;
-    const Plan& plan = ctrl->plan[par];
+    const PeerFlags* inbox = a.inbox + par * n;
     const int64_t st = plan.st, end = plan.end;
     const int ft = (int)(st / TILE), lt = (int)((end - 1) / TILE);
     epi_load(esh, ctrl);  // the stream kernel never writes the control block
@@ -1305,13 +1336,11 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       sa.cnt_out->capped = 0;
     }
     __syncthreads();
-    if (tid < n) {  // H1: one system fence orders K1's pushes and the counts before the epoch
+    if (tid < n) {  // one system fence orders the counts before the epoch
       PeerFlags* slot = a.peer_slot[tid] + par * n;
       st_relaxed_sys_i64(&slot->k, s_k);
       st_relaxed_sys_f64(&slot->norm2, s_n2);
       st_relaxed_sys_i64(&slot->capped, 0);
-      st_relaxed_sys_i64(&slot->st, st);
-      st_relaxed_sys_i64(&slot->end, end);
       asm volatile("fence.acq_rel.sys;" ::: "memory");
       st_relaxed_sys(&slot->count_epoch, a.epoch);
     }
@@ -1339,42 +1368,36 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   }
 
   // ---- work blocks
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // own K1 complete
-  if (tid == 0) s_ok = wait_gate(&a.gate[0], a.epoch, a.err);  // every rank's H1
-  __syncthreads();
-  if (!s_ok) return;
-  if (r == 0) PROBE(8);
   if (tid == 0) {
-    // partition p is held by rank (p - t) mod n (allocator.cpp:92-99); its
-    // range came with the holder's H1
+    // partition table from the replicated plan (allocate_partition,
+    // allocator.cpp:92-99: partition p is held by rank (p - t) mod n; the last
+    // one ends at n_g)
     const int tm = (int)mod_floor(sa.t, n);
-    int64_t off = 0;
+    const exd_topology& tp = plan.topo;
     int32_t tc = 0;
     for (int p = 0; p < n; ++p) {
       const int rk = p - tm < 0 ? p - tm + n : p - tm;
-      const int64_t pst = __ldcg(&inbox[rk].st), pend = __ldcg(&inbox[rk].end);
+      const int64_t pst = tp.blk_pos[p] * tp.sz_blk;
+      const int64_t pend = p == n - 1 ? rc.n_g : (tp.blk_pos[p] + tp.blk_part[p]) * tp.sz_blk;
       s_prank[p] = rk;
-      s_poff[p] = off;
       s_ft[p] = (int32_t)(pst / TILE);
       s_fc[p] = pst / CH;
       s_tcum[p] = tc;
-      off += __ldcg(&inbox[rk].k);
       tc += pend > pst ? (int32_t)((pend - 1) / TILE - pst / TILE + 1) : 0;
     }
-    s_poff[n] = off;
     s_tcum[n] = tc;
     // work blocks per partition, by tiles, at least one each (G >= n)
     for (int p = 0; p <= n; ++p)
       s_bcum[p] = p + (int32_t)(((int64_t)(G - n) * s_tcum[p]) / (tc > 0 ? tc : 1));
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // own K1 complete (e, own runs)
   __syncthreads();
+  if (r == 0) PROBE(8);
 
-  // ---- this block's segment of one partition: contributions out, sums in
   {
     T* __restrict__ e = static_cast<T*>(sa.e);
     T* __restrict__ x = static_cast<T*>(sa.x);
     T* __restrict__ gsum = static_cast<T*>(a.sum);
-    const uint32_t ep = (uint32_t)a.epoch;
     int p = 0;
     while (p + 1 < n && s_bcum[p + 1] <= r) ++p;
     const int rl = r - s_bcum[p], nbl = s_bcum[p + 1] - s_bcum[p];
@@ -1382,19 +1405,82 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int rk = s_prank[p];
     const bool own = rk == me;
     const int ftp = s_ft[p];
-    const int32_t* tcnt = own ? sa.tile_count : a.tile_in[par][rk];
-    const int32_t* ccnt = own ? sa.chunk_count : a.chunk_in[par][rk];
-    const int32_t* sidx = a.stage_in[par][rk];
-    const P* sp = static_cast<const P*>(sa.stage);
     const int t0 = ftp + (int)(((int64_t)ntp * rl) / nbl);
     const int t1 = ftp + (int)(((int64_t)ntp * (rl + 1)) / nbl);
+    const unsigned long long* ccnt_ll = a.chunk_in[par][rk];
+    const unsigned long long* sidx = a.stage_in[par][rk];
+    const P* sp = static_cast<const P*>(sa.stage);
     const int nch = (t1 - t0) * kWarps;
-    int cnt = tid < nch ? __ldcg(&ccnt[t0 * kWarps + tid]) : 0;  // issued before the prefix
-    int64_t running = cta_sum_counts(tcnt, ftp, t0, s_red);  // partition-local index of t0's first entry
+    // chunk counts of the first batch, issued before the base
+    int cnt = 0;
+    unsigned long long cw = 0;
+    if (tid < nch) {
+      if (own) cnt = __ldcg(&sa.chunk_count[t0 * kWarps + tid]);
+      else cw = ld_relaxed_sys_u64(&ccnt_ll[t0 * kWarps + tid]);
+    }
+    // base: the counts of every tile before t0 in partition order (tiles of
+    // partitions < p, then [ftp, t0) of p), own tiles local, others as words
+    int64_t base = 0, poff = 0;  // union position of t0's first entry / of partition p
+    {
+      const int F = s_tcum[p] + (t0 - ftp), Fp = s_tcum[p];
+      int64_t sum = 0, sum_before = 0;
+      for (int f0 = tid; f0 < F; f0 += kSumUnroll * kThreads) {
+        unsigned long long wv[kSumUnroll];
+        const unsigned long long* wp[kSumUnroll];
+#pragma unroll
+        for (int k = 0; k < kSumUnroll; ++k) {
+          const int f = f0 + k * kThreads;
+          wv[k] = (unsigned long long)ep << 32;  // count 0, current epoch
+          wp[k] = nullptr;
+          if (f < F) {
+            int q = 0;
+            while (q + 1 < n && s_tcum[q + 1] <= f) ++q;
+            const int tile = s_ft[q] + (f - s_tcum[q]);
+            const int hr = s_prank[q];
+            if (hr == me) {
+              wv[k] |= (uint32_t)__ldcg(&sa.tile_count[tile]);
+            } else {
+              wp[k] = a.tile_in[par][hr] + tile;
+              wv[k] = ld_relaxed_sys_u64(wp[k]);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kSumUnroll; ++k) {
+          uint32_t c = (uint32_t)wv[k];
+          if ((uint32_t)(wv[k] >> 32) != ep) c = poll_word(wp[k], ep, a.err);
+          sum += c;
+          if (f0 + k * kThreads < Fp) sum_before += c;
+        }
+      }
+      sum = warp_sum(sum);
+      sum_before = warp_sum(sum_before);
+      __shared__ int64_t s_red2[kWarps];
+      if (lane == 0) {
+        s_red[warp] = sum;
+        s_red2[warp] = sum_before;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        base += s_red[w];
+        poff += s_red2[w];
+      }
+      __syncthreads();
+    }
+    if (!own && tid < nch && (uint32_t)(cw >> 32) != ep) cw = poll_word(&ccnt_ll[t0 * kWarps + tid], ep, a.err) | ((unsigned long long)ep << 32);
+    if (!own) cnt = (int)(uint32_t)cw;
     PROBE_MAX(41);
+    int64_t running = base;  // union position of tile t0's first entry
     for (int cb = 0; cb < nch; cb += kThreads) {
       const int nb = nch - cb < kThreads ? nch - cb : kThreads;
-      if (cb) cnt = tid < nb ? __ldcg(&ccnt[t0 * kWarps + cb + tid]) : 0;
+      if (cb) {
+        cnt = 0;
+        if (tid < nb) {
+          if (own) cnt = __ldcg(&sa.chunk_count[t0 * kWarps + cb + tid]);
+          else cnt = (int)poll_word(&ccnt_ll[t0 * kWarps + cb + tid], ep, a.err);
+        }
+      }
       int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1415,25 +1501,36 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       for (int i0 = tid; i0 < btot; i0 += kXUnroll * kThreads) {
         int32_t jj[kXUnroll];
         T vv[kXUnroll];
+        unsigned long long jw[kXUnroll];
+        int64_t src[kXUnroll];
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {
           const int i = i0 + q * kThreads;
           jj[q] = 0;
           vv[q] = T(0);
+          jw[q] = (unsigned long long)ep << 32;
+          src[q] = 0;
           if (i < btot) {
             int lo = 0, hi = nb;  // last chunk k with s_off[k] <= i
             while (hi - lo > 1) {
               const int mid = (lo + hi) >> 1;
               if (s_off[mid] <= i) lo = mid; else hi = mid;
             }
-            const int64_t src = (cbase + lo) * CH + (i - s_off[lo]);
+            src[q] = (cbase + lo) * CH + (i - s_off[lo]);
             if (own) {
-              const P pr = __ldcg(&sp[src]);
+              const P pr = __ldcg(&sp[src[q]]);
               jj[q] = (int32_t)Pair<T>::idx(pr);
               vv[q] = Pair<T>::val(pr);
             } else {
-              jj[q] = __ldcg(&sidx[src]);
+              jw[q] = ld_relaxed_sys_u64(&sidx[src[q]]);
             }
+          }
+        }
+        if (!own) {
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q) {
+            if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[src[q]], ep, a.err);
+            jj[q] = (int32_t)(uint32_t)jw[q];
           }
         }
 #ifdef EXD_PROBE
@@ -1452,14 +1549,14 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         for (int q = 0; q < kXUnroll; ++q) {
           const int i = i0 + q * kThreads;
           if (i >= btot) continue;
-          const int64_t lp = running + i, pos = s_poff[p] + lp;
+          const int64_t pos = running + i;
           for (int rr = 0; rr < n; ++rr)
             if (rr != me)
-              LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[rr]) + pos * W, vv[q], ep);
+              LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rr]) + pos * W, vv[q], ep);
           a.idx_global[pos] = jj[q];
-          if (own) {
-            sa.idx[lp] = jj[q];
-            static_cast<T*>(sa.val)[lp] = vv[q];
+          if (own) {  // this rank's ascending selection (partition-local index)
+            sa.idx[pos - poff] = jj[q];
+            static_cast<T*>(sa.val)[pos - poff] = vv[q];
           } else {
             e[jj[q]] = T(0);  // own partition was cleared by the stream kernel
           }
@@ -1480,8 +1577,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
               pv[q][b] = vv[q];
               ok[q][b] = true;
               if (rr < n && rr != me && i0 + q * kThreads < btot)
-                ok[q][b] = LL<T>::get(static_cast<const unsigned long long*>(a.contrib_in[rr]) +
-                                          (s_poff[p] + running + i0 + q * kThreads) * W, ep, pv[q][b]);
+                ok[q][b] = LL<T>::get(static_cast<const unsigned long long*>(a.contrib_in[par][rr]) +
+                                          (running + i0 + q * kThreads) * W, ep, pv[q][b]);
             }
 #pragma unroll
           for (int q = 0; q < kXUnroll; ++q)
@@ -1489,7 +1586,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
             for (int b = 0; b < kXPeers; ++b) {
               if (ok[q][b]) continue;
               const unsigned long long* w = static_cast<const unsigned long long*>(
-                  a.contrib_in[r0 + b]) + (s_poff[p] + running + i0 + q * kThreads) * W;
+                  a.contrib_in[par][r0 + b]) + (running + i0 + q * kThreads) * W;
               const unsigned long long tw = gtime_ns();
               unsigned spins = 0;
               while (!LL<T>::get(w, ep, pv[q][b])) {
@@ -1511,7 +1608,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         for (int q = 0; q < kXUnroll; ++q) {
           const int i = i0 + q * kThreads;
           if (i >= btot) continue;
-          gsum[s_poff[p] + running + i] = sv[q];
+          gsum[running + i] = sv[q];
           x[jj[q]] = apply_update<T>(xv[q], sv[q], n);
         }
       }
@@ -2045,9 +2142,10 @@ cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s) {
 }
 
 cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s) {
-  // every block must be resident (in-kernel arrive counter): 2 per SM + block 0
+  // 3 per SM, all resident (__launch_bounds__(kThreads, 3)): block 0 + 3*SMs - 1
+  // work blocks, so a dense tile range is split finely enough for one pass
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p2p_blocks() + 1);
+  cfg.gridDim = dim3(p2p_blocks() / 2 * 3);
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
