@@ -262,18 +262,23 @@ def run_ours(args):
         dist.broadcast(t, src=0)
         extra = [int(t[0])]
     run_steps(extra[0])
-    eng.reset_kernel_stats()
-    barrier()
-    # one untimed step right after the host barrier (the ranks leave it tens of
-    # us apart; the step's in-kernel exchange realigns them), then the device sync
-    run_steps(1)
-    torch.cuda.synchronize()
-    launches0 = eng.kernel_stats()["kernel_launches"]
-
     # ---- value: K steps, each bracketed by events on the engine's stream, L2
     # flushed before each (flush excluded). Per-kernel profiling is OFF here so
     # the stream->finish programmatic launch overlap is what gets timed.
     eng.set_profile(False)
+    eng.reset_kernel_stats()
+    run_steps(1)
+    per_step_launches = eng.kernel_stats()["kernel_launches"]
+    launches0 = per_step_launches + 2 * per_step_launches  # the two aligning steps below
+    barrier()
+    # two untimed steps enqueued right behind the host barrier, with no host
+    # sync before the timed ones: the ranks leave the barrier up to ~0.2 ms
+    # apart, and the steps' in-kernel exchange realigns their streams
+    for _ in range(2):
+        src.gradient(i, rank, bufs[i % POOL], "f32", eng.stream())
+        eng.step_async([bufs[i % POOL]])
+        i += 1
+
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     recs = []
