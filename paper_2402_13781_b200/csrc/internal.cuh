@@ -145,8 +145,9 @@ struct PeerFlags {                   // inbox[src] on the receiver
   double norm2;
   unsigned long long contrib_epoch;  // src's contributions of step epoch-1 are readable
   int64_t capped;
-  int64_t st, end;                   // src's partition range of step epoch-1 (push-reduce)
-  unsigned long long pad[9];         // 128 B: one slot per line
+  int64_t st, end;                   // (unused by push-reduce)
+  unsigned long long ll[3];          // push-reduce: {k, epoch}, {norm2 lo, epoch}, {norm2 hi, epoch}
+  unsigned long long pad[6];         // 128 B: one slot per line
 };
 
 struct P2PArgs {

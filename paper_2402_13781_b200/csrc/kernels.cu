@@ -1336,24 +1336,19 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       sa.cnt_out->capped = 0;
     }
     __syncthreads();
-    if (tid < n) {  // one system fence orders the counts before the epoch
+    if (tid < n) {  // {k, epoch} and the two halves of ||e||^2 as words: no fence
       PeerFlags* slot = a.peer_slot[tid] + par * n;
-      st_relaxed_sys_i64(&slot->k, s_k);
-      st_relaxed_sys_f64(&slot->norm2, s_n2);
-      st_relaxed_sys_i64(&slot->capped, 0);
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      st_relaxed_sys(&slot->count_epoch, a.epoch);
+      const unsigned long long eph = (unsigned long long)ep << 32;
+      const unsigned long long nb = (unsigned long long)__double_as_longlong(s_n2);
+      st_relaxed_sys_u64(&slot->ll[0], eph | (uint32_t)s_k);
+      st_relaxed_sys_v2u64(&slot->ll[1], eph | (nb & 0xffffffffull), eph | (nb >> 32));
     }
-    if (tid == 0) {
-      PROBE(1);
-      s_ok = poll_inbox_open_gate(inbox, n, false, a.epoch, &a.gate[0], a.err);
-      PROBE(2);
-    }
-    __syncthreads();
-    if (!s_ok) return;
+    if (tid == 0) PROBE(1);
     for (int q = tid; q < n; q += kThreads) {
-      const int64_t k = __ldcg(&inbox[q].k);
-      const double n2 = __ldcg(&inbox[q].norm2);
+      const int64_t k = poll_word(&inbox[q].ll[0], ep, a.err);
+      const unsigned long long lo = poll_word(&inbox[q].ll[1], ep, a.err);
+      const unsigned long long hi = poll_word(&inbox[q].ll[2], ep, a.err);
+      const double n2 = __longlong_as_double((long long)((hi << 32) | lo));
       esh.k_rank[q] = k;
       esh.norm2[q] = n2;
       esh.capped[q] = 0;
@@ -1362,6 +1357,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       a.counts_all[q].capped = 0;
     }
     __syncthreads();
+    if (tid == 0) PROBE(2);
     epi_run_store(esh, ctrl, rc, a.rec);
     if (tid == 0) PROBE(4);
     return;
