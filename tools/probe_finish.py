@@ -44,3 +44,16 @@ for i in range(5):
     rows.append(row)
 for r in rows:
     print("  ".join(f"{k}={v:.1f}" for k, v in sorted(r.items(), key=lambda kv: kv[1])))
+# back to back (no flush, no sync between steps): the gap from the finish
+# kernel's last stamp of step t to the stream kernel's first CTA of step t+1
+xs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+for i in range(50):
+    xs2[i][0].record(xs)
+    eng.step_async(pool[i % 2])
+    xs2[i][1].record(xs)
+eng.sync()
+buf = (C.c_uint64 * 64)()
+L.exd_debug_probe(buf)
+us = sorted(a_.elapsed_time(b_) * 1e3 for a_, b_ in xs2)
+print(f"back-to-back: step median {us[25]:.1f} us; prev step k1 -> K2_END {(buf[52] - buf[51]) / 1e3:.1f} us, "
+      f"K2_END -> this k1 {(buf[16] - buf[52]) / 1e3:.1f} us")
