@@ -372,7 +372,7 @@ def run_ours(args):
     peak, peak_src = peaks()
     traffic = ncu_traffic()
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "kernel": "select_kernel<float,kFused>",
+            "frac": achieved / peak, "traffic": traffic, "kernel": "stream_kernel<float,kFused> (K1: accumulate + select + stage)",
             "kernel_ms": sel_ms, "finish_kernel_ms": fin_ms,
             "algorithmic_bytes_per_launch": alg_bytes,
             "peak_source": peak_src, "share_of_step": sel_ms / ms}

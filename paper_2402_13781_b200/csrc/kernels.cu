@@ -1,18 +1,23 @@
 // kernels.cu — the sm_100a kernels of the ExDyna sparsify+sync path.
 //
-//   select_kernel   (K1+K2) fused accumulate e <- e + eta*g over the full
-//                   vector, |acc| >= delta test over the worker's exclusive
-//                   partition, per-block counts, and ordered single-pass
-//                   compaction to (int32 index, value) pairs by decoupled
-//                   look-back; own selected residuals are zeroed in the same
-//                   pass. For n == 1 it also applies x -= g/n and runs the
-//                   control epilogue, so a whole step is one launch.
-//   union_kernel    (K4+K5) union in partition order + contribution gather +
-//                   residual clear at the union.
-//   allreduce_local rank-order sum of n in-process contributions (K6, sim mode).
-//   finalize_kernel (K7+K9) x scatter, threshold scaling, record, next plan.
+//   stream_kernel   (K1) accumulate e <- e + eta*g over the full vector,
+//                   |acc| >= delta over the worker's exclusive partition,
+//                   own selected residuals zeroed, the selection staged in
+//                   order per warp chunk as (index, value) pairs, per-block
+//                   counts. PUSH variant (one rank per GPU): the staged runs
+//                   and counts also go to every peer's inbox.
+//   finish_kernel   (K2) per-chunk counts -> global offsets, dense ascending
+//                   idx/val lists; for n == 1 also x -= g/n and the control
+//                   epilogue, so a step is two launches chained by PDL.
+//   exchange_kernel (K2 + sync, one rank per GPU, push-reduce) union in
+//                   partition order, contributions out and in as {value,
+//                   epoch} words, rank-order sum, x -= g/n, epilogue.
+//   p2p_sync        (pull-reduce peer sync) and union / allreduce_local /
+//                   finalize (in-process workers, NCCL path): K4-K9.
+//   cap_kernel      density cap (selector.cpp:44-61).
 //   quantile        (K8) radix select of the (1-d)-quantile of |acc| at t = 0.
 //   synthetic       device GradientSource (workloads.cpp:62-85).
+//   verify / hash / conservation kernels: the reference's debug invariants.
 //
 // Reference lines are cited at each kernel. Everything here is HBM- or
 // latency-bound integer/byte work: there is no GEMM to put on tcgen05, so the
