@@ -36,6 +36,13 @@ def test_two_ranks_push_reduce_f64_vs_oracle():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["p2p", "p2p-pull"])
+def test_two_ranks_sparse_selection(sync):
+    # k = 40 over 400k elements: partitions that select nothing, one-entry chunks
+    _run(2, "--sync", sync, "--n_g", "400001", "--density", "0.0001", "--steps", "16", port=29582)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 def test_two_ranks_density_cap():
     _run(2, "--sync", "p2p", "--cap", "0.01", "--steps", "10", port=29578)
 
@@ -50,3 +57,9 @@ def test_replica_divergence_detected_across_gpus(sync):
 @pytest.mark.parametrize("sync", ["p2p", "p2p-pull"])
 def test_four_ranks_p2p_rank_order_sum_is_bit_exact(sync):
     _run(4, "--sync", sync, "--steps", "12", port=29580)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_push_reduce_dense_and_sparse():
+    _run(4, "--sync", "p2p", "--density", "0.1", "--steps", "8", port=29583)
+    _run(4, "--sync", "p2p", "--n_g", "400001", "--density", "0.0002", "--steps", "8", port=29584)

@@ -23,7 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n_g", type=int, default=200_003)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--d", type=float, default=0.01)
+    ap.add_argument("--density", "--d", dest="d", type=float, default=0.01)
     ap.add_argument("--skew", type=int, default=1)
     ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p", "p2p-pull"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
