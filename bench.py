@@ -389,6 +389,19 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    # sync stage over NVLink (push-reduce): algorithmic bytes each GPU stores into
+    # its peers' inboxes per step, against the exchange kernel's event time
+    nvlink = None
+    if n > 1 and eng.sync_mode() == "p2p":
+        tiles_own = (N_G / n) / 4096.0
+        out_b = (n - 1) * (8 * k_own + 72 * tiles_own + 8 * kp)
+        nvlink = {"bytes_out_per_gpu_per_step": out_b, "sync_kernel_ms": fin_ms,
+                  "achieved_gbs": out_b / (fin_ms * 1e-3) / 1e9, "peak_gbs": 900.0,
+                  "frac": out_b / (fin_ms * 1e-3) / 1e9 / 900.0,
+                  "note": "latency-bound at this size (~1 MB per GPU per step): the exchange "
+                          "kernel's time is round trips, not link bandwidth; bytes = staged-index "
+                          "and count words pushed by the stream kernel + one 8 B contribution "
+                          "word per union entry, per peer"}
     cfg_line = workload(n)
     if n > 1:
         cfg_line["sync"] = {
@@ -406,6 +419,7 @@ def run_ours(args):
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * N_G * n,
                 "d2h_bytes_per_step": C.sizeof(A.exd_record) * n},
         "gpu_launches": launches,
+        "nvlink": nvlink,
         "clocks": clk,
         "records": {"k_prime_mean": kp, "f_t_mean": statistics.mean(r.f_t for r in recs),
                     "density_mean": statistics.mean(r.density for r in recs),
