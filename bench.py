@@ -406,7 +406,7 @@ def run_ours(args):
     if n > 1:
         cfg_line["sync"] = {
             "p2p": "NVLink peer memory, push-reduce (lists pushed during the stream, "
-                   "{value, epoch} contribution words; one handshake, no host wait)",
+                   "everything as {payload, epoch} words; no handshake, no host wait)",
             "p2p-pull": "NVLink peer memory, pull-reduce (lists pushed, contributions pulled)",
             "nccl": "NCCL all-gather/all-reduce + one host wait"}[eng.sync_mode()]
     line = {
