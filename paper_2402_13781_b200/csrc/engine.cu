@@ -740,7 +740,6 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   o.rec = wk.rec_dev + (h->t % kRecRing);
   o.epoch = (unsigned long long)h->t + 1;
   o.err = h->p2p_err_dev;
-  o.gate = h->p2p_gate;
   o.me = wk.rank;
   return o;
 }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "control.cuh"
@@ -145,10 +146,12 @@ struct PeerFlags {                   // inbox[src] on the receiver
   double norm2;
   unsigned long long contrib_epoch;  // src's contributions of step epoch-1 are readable
   int64_t capped;
-  int64_t st, end;                   // (unused by push-reduce)
+  unsigned long long pad0[2];
   unsigned long long ll[3];          // push-reduce: {k, epoch}, {norm2 lo, epoch}, {norm2 hi, epoch}
   unsigned long long pad[6];         // 128 B: one slot per line
 };
+static_assert(sizeof(PeerFlags) == 128, "one flag slot per 128 B line");
+static_assert(offsetof(PeerFlags, ll) % 16 == 8, "ll[1..2] is one 16 B vector store");
 
 struct P2PArgs {
   PeerFlags* inbox;                  // [n] own inbox flag slots (local)
@@ -193,7 +196,6 @@ struct ExchangeArgs {
   RawRecord* rec;
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
-  unsigned long long* gate;          // [3] local gate words ([0]: H1 seen)
   int32_t me;
 };
 
