@@ -594,9 +594,11 @@ int setup_p2p(exd_engine* h) {
       h->stage_in[par].assign(n, nullptr);
       h->chunk_in[par].assign(n, nullptr);
       h->tile_in[par].assign(n, nullptr);
-      for (int r = 0; r < n; ++r) {
-        if (r == me) continue;
-        // my slots in rank r's inbox, and rank r's slots in mine
+      // my slots in every rank's inbox, the peers first and my own last (the
+      // exchange kernel reads its own partition's runs and counts as words
+      // too, so it need not wait for the stream kernel to look them up)
+      for (int q = 1; q <= n; ++q) {
+        const int r = (me + q) % n;
         const size_t sm = (size_t)(par * n + me), sr = (size_t)(par * n + r);
         using W = unsigned long long;
         h->push_stage[par].push_back(reinterpret_cast<W*>(base[r] + off_st + stage_b * sm));
@@ -707,7 +709,7 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   // with a cap the list is pushed only after it is trimmed (cap kernel)
   a.push_idx = (h->p2p && !h->xchg && h->cap == 0) ? h->d_push : nullptr;
   a.npush = (h->p2p && !h->xchg && h->cap == 0) ? h->n - 1 : 0;
-  a.k1_npush = h->xchg ? h->n - 1 : 0;
+  a.k1_npush = h->xchg ? h->n : 0;  // every peer, then this rank's own inbox
   const int par = (int)(h->t & 1);  // this step's parity slots
   for (int q = 0; q < a.k1_npush; ++q) {
     a.push_stage[q] = h->push_stage[par][q];

@@ -105,9 +105,9 @@ struct SelectArgs {
   // P2P push-reduce: the stream kernel's pushes into every peer's inbox (by
   // value: kernel parameters are constant-bank reads, no pointer round trip)
   // ({payload, epoch} words, this step's parity)
-  unsigned long long* push_stage[EXD_MAX_WORKERS - 1];  // [k1_npush] my staged-index slot
-  unsigned long long* push_chunk[EXD_MAX_WORKERS - 1];  // [k1_npush] my per-chunk count slot
-  unsigned long long* push_tile[EXD_MAX_WORKERS - 1];   // [k1_npush] my per-tile count slot
+  unsigned long long* push_stage[EXD_MAX_WORKERS];  // [k1_npush] my staged-index slot (peers, then own)
+  unsigned long long* push_chunk[EXD_MAX_WORKERS];  // [k1_npush] my per-chunk count slot
+  unsigned long long* push_tile[EXD_MAX_WORKERS];   // [k1_npush] my per-tile count slot
   int32_t k1_npush;             // 0: no pushes
 };
 

@@ -1399,7 +1399,10 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     for (int p = 0; p <= n; ++p)
       s_bcum[p] = p + (int32_t)(((int64_t)(G - n) * s_tcum[p]) / (tc > 0 ? tc : 1));
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // own K1 complete (e, own runs)
+  // No griddepcontrol.wait yet: the partition's runs and counts arrive as words
+  // (this rank's own too), so the lookups below overlap this rank's stream
+  // kernel draining its remote stores. The wait comes before the first access
+  // to what the stream kernel writes locally (e, the staged values).
   __syncthreads();
   if (r == 0) PROBE(8);
 
@@ -1422,13 +1425,10 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int nch = (t1 - t0) * kWarps;
     // chunk counts of the first batch, issued before the base
     int cnt = 0;
-    unsigned long long cw = 0;
-    if (tid < nch) {
-      if (own) cnt = __ldcg(&sa.chunk_count[t0 * kWarps + tid]);
-      else cw = ld_relaxed_sys_u64(&ccnt_ll[t0 * kWarps + tid]);
-    }
+    unsigned long long cw = (unsigned long long)ep << 32;
+    if (tid < nch) cw = ld_relaxed_sys_u64(&ccnt_ll[t0 * kWarps + tid]);
     // base: the counts of every tile before t0 in partition order (tiles of
-    // partitions < p, then [ftp, t0) of p), own tiles local, others as words
+    // partitions < p, then [ftp, t0) of p), as words
     int64_t base = 0, poff = 0;  // union position of t0's first entry / of partition p
     {
       const int F = s_tcum[p] + (t0 - ftp), Fp = s_tcum[p];
@@ -1445,13 +1445,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
             int q = 0;
             while (q + 1 < n && s_tcum[q + 1] <= f) ++q;
             const int tile = s_ft[q] + (f - s_tcum[q]);
-            const int hr = s_prank[q];
-            if (hr == me) {
-              wv[k] |= (uint32_t)__ldcg(&sa.tile_count[tile]);
-            } else {
-              wp[k] = a.tile_in[par][hr] + tile;
-              wv[k] = ld_relaxed_sys_u64(wp[k]);
-            }
+            wp[k] = a.tile_in[par][s_prank[q]] + tile;
+            wv[k] = ld_relaxed_sys_u64(wp[k]);
           }
         }
 #pragma unroll
@@ -1477,18 +1472,16 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       }
       __syncthreads();
     }
-    if (!own && tid < nch && (uint32_t)(cw >> 32) != ep) cw = poll_word(&ccnt_ll[t0 * kWarps + tid], ep, a.err) | ((unsigned long long)ep << 32);
-    if (!own) cnt = (int)(uint32_t)cw;
+    if (tid < nch && (uint32_t)(cw >> 32) != ep)
+      cw = poll_word(&ccnt_ll[t0 * kWarps + tid], ep, a.err) | ((unsigned long long)ep << 32);
+    cnt = (int)(uint32_t)cw;
     PROBE_MAX(41);
     int64_t running = base;  // union position of tile t0's first entry
     for (int cb = 0; cb < nch; cb += kThreads) {
       const int nb = nch - cb < kThreads ? nch - cb : kThreads;
       if (cb) {
         cnt = 0;
-        if (tid < nb) {
-          if (own) cnt = __ldcg(&sa.chunk_count[t0 * kWarps + cb + tid]);
-          else cnt = (int)poll_word(&ccnt_ll[t0 * kWarps + cb + tid], ep, a.err);
-        }
+        if (tid < nb) cnt = (int)poll_word(&ccnt_ll[t0 * kWarps + cb + tid], ep, a.err);
       }
       int incl = cnt;
 #pragma unroll
@@ -1526,22 +1519,16 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
               if (s_off[mid] <= i) lo = mid; else hi = mid;
             }
             src[q] = (cbase + lo) * CH + (i - s_off[lo]);
-            if (own) {
-              const P pr = __ldcg(&sp[src[q]]);
-              jj[q] = (int32_t)Pair<T>::idx(pr);
-              vv[q] = Pair<T>::val(pr);
-            } else {
-              jw[q] = ld_relaxed_sys_u64(&sidx[src[q]]);
-            }
+            jw[q] = ld_relaxed_sys_u64(&sidx[src[q]]);
           }
         }
-        if (!own) {
 #pragma unroll
-          for (int q = 0; q < kXUnroll; ++q) {
-            if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[src[q]], ep, a.err);
-            jj[q] = (int32_t)(uint32_t)jw[q];
-          }
+        for (int q = 0; q < kXUnroll; ++q) {
+          if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[src[q]], ep, a.err);
+          jj[q] = (int32_t)(uint32_t)jw[q];
         }
+        // from here on: what this rank's stream kernel wrote (e, staged values)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef EXD_PROBE
         if (jj[0] == 0x7fffffff) g_probe[63] = 1;  // force the loads before the stamp
         PROBE_MAX(42);
@@ -1550,7 +1537,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {
           if (i0 + q * kThreads >= btot) continue;
-          if (!own) vv[q] = e[jj[q]];
+          vv[q] = own ? Pair<T>::val(__ldcg(&sp[src[q]])) : e[jj[q]];
           xv[q] = x[jj[q]];
         }
         // own contribution out (every peer's inbox), union entry, residual clear
