@@ -1527,19 +1527,21 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
           if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[src[q]], ep, a.err);
           jj[q] = (int32_t)(uint32_t)jw[q];
         }
+        // x is not written by the stream kernel (the previous step's kernels
+        // completed before it started): gather it before the wait
+        T xv[kXUnroll];
+#pragma unroll
+        for (int q = 0; q < kXUnroll; ++q)
+          if (i0 + q * kThreads < btot) xv[q] = x[jj[q]];
         // from here on: what this rank's stream kernel wrote (e, staged values)
         asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef EXD_PROBE
         if (jj[0] == 0x7fffffff) g_probe[63] = 1;  // force the loads before the stamp
         PROBE_MAX(42);
 #endif
-        T xv[kXUnroll];
 #pragma unroll
-        for (int q = 0; q < kXUnroll; ++q) {
-          if (i0 + q * kThreads >= btot) continue;
-          vv[q] = own ? Pair<T>::val(__ldcg(&sp[src[q]])) : e[jj[q]];
-          xv[q] = x[jj[q]];
-        }
+        for (int q = 0; q < kXUnroll; ++q)
+          if (i0 + q * kThreads < btot) vv[q] = own ? Pair<T>::val(__ldcg(&sp[src[q]])) : e[jj[q]];
         // own contribution out (every peer's inbox), union entry, residual clear
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {
