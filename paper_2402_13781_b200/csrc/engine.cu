@@ -17,6 +17,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -243,6 +244,9 @@ struct exd_engine {
   std::vector<PeerFlags*> slot_host;                   // [n] my parity-0 flag slot in every rank's inbox
   std::vector<const unsigned long long*> stage_in[2], chunk_in[2], tile_in[2];  // [n] inbox slots by source
   std::vector<void*> contrib_out[2];                   // [n] my contribution slot in every inbox
+  std::vector<void*> sum_out[2];                       // [n] the holder-sum slot of every inbox
+  const void* sum_in[2] = {nullptr, nullptr};          // own holder-sum slots
+  bool holder_sum = false;                             // n >= 4 (EXD_HOLDER_SUM=0/1 overrides)
   std::vector<const void*> contrib_in[2];              // [n] contribution slots by source (local)
   unsigned long long* rep_hash = nullptr;  // [4 * (n + 1)]: own words, then all ranks' words
   int32_t* recv = nullptr;
@@ -527,7 +531,7 @@ int setup_p2p(exd_engine* h) {
       off_ch = off_st + stage_b * 2 * n;
       off_ti = off_ch + chunk_b * 2 * n;
       off_xc = off_ti + tile_b * 2 * n;
-      total = off_xc + xcon_b * 2 * n;
+      total = off_xc + xcon_b * 2 * n + xcon_b * 2;  // + the holder-sum slots [2]
     } else {
       // pull-reduce: flags[n] | lists[n][cap_part] | contrib[2][n_g]
       flags_b = al(sizeof(PeerFlags) * (size_t)n);
@@ -610,12 +614,19 @@ int setup_p2p(exd_engine* h) {
       }
       h->contrib_out[par].assign(n, nullptr);
       h->contrib_in[par].assign(n, nullptr);
+      h->sum_out[par].assign(n, nullptr);
+      h->sum_in[par] = own + off_xc + xcon_b * (size_t)(2 * n + par);
       for (int r = 0; r < n; ++r) {
         h->contrib_out[par][r] = base[r] + off_xc + xcon_b * (size_t)(par * n + me);
         h->contrib_in[par][r] = own + off_xc + xcon_b * (size_t)(par * n + r);
+        h->sum_out[par][r] = base[r] + off_xc + xcon_b * (size_t)(2 * n + par);
       }
     }
     for (int r = 0; r < n; ++r) h->slot_host[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
+    // every rank must agree: the choice depends only on n (and the same
+    // environment on every rank)
+    h->holder_sum = n >= 4;
+    if (const char* hs = std::getenv("EXD_HOLDER_SUM")) h->holder_sum = hs[0] == '1';
   }
   std::vector<PeerFlags*> slot(n);
   std::vector<const int32_t*> lists(n);
@@ -723,6 +734,9 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   Worker& wk = h->w[0];
   ExchangeArgs o{};
   o.s = sa;
+  o.holder_sum = h->holder_sum ? 1 : 0;
+  o.sum_in[0] = h->sum_in[0];
+  o.sum_in[1] = h->sum_in[1];
   o.inbox = h->inbox;
   for (int r = 0; r < h->n; ++r) {
     o.peer_slot[r] = h->slot_host[r];
@@ -734,6 +748,7 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
     for (int par = 0; par < 2; ++par) {
       o.contrib_out[par][r] = h->contrib_out[par][r];
       o.contrib_in[par][r] = h->contrib_in[par][r];
+      o.sum_out[par][r] = h->sum_out[par][r];
     }
   }
   o.idx_global = wk.idx_global;

@@ -190,6 +190,12 @@ struct ExchangeArgs {
   const unsigned long long* tile_in[2][EXD_MAX_WORKERS];
   void* contrib_out[2][EXD_MAX_WORKERS];        // [parity] my {value, epoch} slot in every inbox
   const void* contrib_in[2][EXD_MAX_WORKERS];   // [parity] {value, epoch} slots by source (local)
+  // holder sum (n >= 4): contributions go to the partition's holder only, which
+  // sums them and sends the sums to everyone: 2(n-1)/n instead of n-1 words
+  // per union entry leave each GPU, for one more NVLink flight
+  int32_t holder_sum;
+  void* sum_out[2][EXD_MAX_WORKERS];            // [parity] the sum slot of every rank's inbox
+  const void* sum_in[2];                        // [parity] own sum slot (local)
   int32_t* idx_global;               // [k'] union, partition order
   void* sum;                         // [k'] aggregated values (T)
   CountRec* counts_all;              // [n] local copy of the gathered counts

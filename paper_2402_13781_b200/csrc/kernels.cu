@@ -1416,6 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int ntp = s_tcum[p + 1] - s_tcum[p];
     const int rk = s_prank[p];
     const bool own = rk == me;
+    const bool hs = a.holder_sum != 0;
     const int ftp = s_ft[p];
     const int t0 = ftp + (int)(((int64_t)ntp * rl) / nbl);
     const int t1 = ftp + (int)(((int64_t)ntp * (rl + 1)) / nbl);
@@ -1548,9 +1549,13 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
           const int i = i0 + q * kThreads;
           if (i >= btot) continue;
           const int64_t pos = running + i;
-          for (int rr = 0; rr < n; ++rr)
-            if (rr != me)
-              LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rr]) + pos * W, vv[q], ep);
+          if (!hs) {  // to every peer: each rank sums all n itself
+            for (int rr = 0; rr < n; ++rr)
+              if (rr != me)
+                LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rr]) + pos * W, vv[q], ep);
+          } else if (!own) {  // to the partition's holder, which sums and sends the sum back
+            LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rk]) + pos * W, vv[q], ep);
+          }
           a.idx_global[pos] = jj[q];
           if (own) {  // this rank's ascending selection (partition-local index)
             sa.idx[pos - poff] = jj[q];
@@ -1562,9 +1567,10 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
 #ifdef EXD_PROBE
         PROBE_MAX(43);
 #endif
-        // the peers' contributions for the same positions; rank-order sum
+        // the peers' contributions for the same positions; rank-order sum (the
+        // holder only, under the holder sum; the others poll the holder's sum)
         T sv[kXUnroll];
-        for (int r0 = 0; r0 < n; r0 += kXPeers) {
+        for (int r0 = 0; r0 < ((!hs || own) ? n : 0); r0 += kXPeers) {
           T pv[kXUnroll][kXPeers];
           bool ok[kXUnroll][kXPeers];
 #pragma unroll
@@ -1601,6 +1607,33 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
 #pragma unroll
             for (int b = 0; b < kXPeers; ++b)
               if (r0 + b < n) sv[q] = r0 + b == 0 ? pv[q][b] : sv[q] + pv[q][b];
+        }
+        if (hs && own) {  // the holder sends the sums to every peer
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q) {
+            if (i0 + q * kThreads >= btot) continue;
+            const int64_t pos = running + i0 + q * kThreads;
+            for (int rr = 0; rr < n; ++rr)
+              if (rr != me)
+                LL<T>::put(static_cast<unsigned long long*>(a.sum_out[par][rr]) + pos * W, sv[q], ep);
+          }
+        } else if (hs) {  // everyone else polls the holder's sum
+#pragma unroll
+          for (int q = 0; q < kXUnroll; ++q) {
+            if (i0 + q * kThreads >= btot) continue;
+            const unsigned long long* w = static_cast<const unsigned long long*>(a.sum_in[par]) +
+                                          (running + i0 + q * kThreads) * W;
+            const unsigned long long tw = gtime_ns();
+            unsigned spins = 0;
+            while (!LL<T>::get(w, ep, sv[q])) {
+              if ((++spins & 255u) == 0 &&
+                  (gtime_ns() - tw > 20000000000ull || *(volatile unsigned int*)a.err)) {
+                atomicExch(a.err, 1u);
+                break;
+              }
+              __nanosleep(20);
+            }
+          }
         }
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {

@@ -15,11 +15,12 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(nproc, *args, port=29577):
+def _run(nproc, *args, port=29577, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tools", "dist_check.py"), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "PASS" in r.stdout
 
@@ -28,6 +29,13 @@ def _run(nproc, *args, port=29577):
 @pytest.mark.parametrize("sync", ["p2p", "p2p-pull", "nccl"])
 def test_two_ranks_bit_exact_vs_oracle(sync):
     _run(2, "--sync", sync, "--steps", "12")
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("holder_sum", ["0", "1"])
+def test_two_ranks_push_reduce_holder_sum_switch(holder_sum):
+    # the holder-sum exchange is the default from n = 4; force both ways at n = 2
+    _run(2, "--sync", "p2p", "--steps", "12", port=29585, env={"EXD_HOLDER_SUM": holder_sum})
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
@@ -63,3 +71,9 @@ def test_four_ranks_p2p_rank_order_sum_is_bit_exact(sync):
 def test_four_ranks_push_reduce_dense_and_sparse():
     _run(4, "--sync", "p2p", "--density", "0.1", "--steps", "8", port=29583)
     _run(4, "--sync", "p2p", "--n_g", "400001", "--density", "0.0002", "--steps", "8", port=29584)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_push_reduce_all_push():
+    _run(4, "--sync", "p2p", "--steps", "12", port=29586, env={"EXD_HOLDER_SUM": "0"})
+    _run(4, "--sync", "p2p", "--dtype", "f64", "--steps", "6", port=29587)
