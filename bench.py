@@ -394,14 +394,17 @@ def run_ours(args):
     nvlink = None
     if n > 1 and eng.sync_mode() == "p2p":
         tiles_own = (N_G / n) / 4096.0
-        out_b = (n - 1) * (8 * k_own + 72 * tiles_own + 8 * kp)
+        holder = (n >= 4) if "EXD_HOLDER_SUM" not in os.environ else os.environ["EXD_HOLDER_SUM"] == "1"
+        words = (kp - k_own) + (n - 1) * k_own if holder else (n - 1) * kp  # contribution/sum words out
+        out_b = (n - 1) * (8 * k_own + 72 * tiles_own) + 8 * words
         nvlink = {"bytes_out_per_gpu_per_step": out_b, "sync_kernel_ms": fin_ms,
                   "achieved_gbs": out_b / (fin_ms * 1e-3) / 1e9, "peak_gbs": 900.0,
                   "frac": out_b / (fin_ms * 1e-3) / 1e9 / 900.0,
                   "note": "latency-bound at this size (~1 MB per GPU per step): the exchange "
                           "kernel's time is round trips, not link bandwidth; bytes = staged-index "
-                          "and count words pushed by the stream kernel + one 8 B contribution "
-                          "word per union entry, per peer"}
+                          "and count words pushed by the stream kernel + 8 B contribution words "
+                          "(to every peer, or to the holder and sums back for n >= 4)",
+                  "holder_sum": holder}
     cfg_line = workload(n)
     if n > 1:
         cfg_line["sync"] = {
