@@ -224,6 +224,19 @@ int exd_gather_stats_of(const int64_t* k_rank, int32_t n, exd_gather_stats* out)
  * |mags| (dtype elements, device pointer); result written to *out (host). */
 int exd_initial_threshold_device(const void* mags_dev, int64_t m, int32_t dtype,
                                  double d, double* out);
+/* Baseline sparsifiers, baselines.hpp:25-34 / baselines.cpp:26-46 (SURVEY
+ * §8f row f4), over a device vector acc (dtype elements, n_g long). Indices
+ * are ascending int32 written to idx_dev (device, capacity cap); enqueued on
+ * cuda_stream, which the call synchronises.
+ * topk_select: exactly k indices, largest |acc| first, ties toward the lower
+ * index; EXD_EINVAL "topk_select: k out of range" unless 1 <= k <= n_g. */
+int exd_topk_select_device(const void* acc_dev, int64_t n_g, int32_t dtype, int64_t k,
+                           int32_t* idx_dev, int64_t cap, void* cuda_stream);
+/* hard_threshold_select: {j : |acc[j]| >= fixed_delta} compared in fp64;
+ * *count (host) gets the full count, at most cap indices are written. */
+int exd_hard_threshold_select_device(const void* acc_dev, int64_t n_g, int32_t dtype,
+                                     double fixed_delta, int32_t* idx_dev, int64_t cap,
+                                     int64_t* count, void* cuda_stream);
 /* synthetic_gradient, workloads.cpp:62-85, generated on device (dtype). */
 int exd_synthetic_gradient(const exd_stream_spec* spec, int64_t t, int32_t rank,
                            int32_t dtype, void* out_dev, void* cuda_stream);

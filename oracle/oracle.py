@@ -103,6 +103,8 @@ def ref():
         L.ref_initial_threshold.argtypes = [PD, C.c_int64, C.c_double, PD]
         L.ref_all_gather.argtypes = [PI64, PI64, C.c_int32, C.POINTER(A.exd_gather_stats),
                                      PI64, PI64, PI64]
+        L.ref_topk_select.argtypes = [PD, C.c_int64, C.c_int64, PI64]
+        L.ref_hard_threshold_select.argtypes = [PD, C.c_int64, C.c_double, PI64, PI64]
         L.ref_synthetic_gradient.argtypes = [C.POINTER(A.exd_stream_spec), C.c_int64, C.c_int32, PD]
         L.ref_engine_create.restype = P
         L.ref_engine_create.argtypes = [C.POINTER(A.exd_config), C.POINTER(A.exd_options), C.c_int32]
@@ -226,6 +228,43 @@ def synthetic_gradient_ref(spec, t, rank):
     if rc:
         raise CheckError(rc, ref().ref_last_error().decode())
     return out
+
+
+# ---- baseline sparsifiers: numpy restatement -----------
+def topk_select_np(acc, k):
+    """baselines.cpp:26-41: the k largest |acc| under the total order
+    (|a| desc, index asc) of its nth_element comparator (:33-37), ascending."""
+    n = acc.shape[0]
+    if k < 1 or k > n:
+        raise ValueError("topk_select: k out of range")
+    mag = np.abs(acc.astype(np.float64))
+    order = np.lexsort((np.arange(n), -mag))
+    return np.sort(order[:k]).astype(np.int64)
+
+
+def hard_threshold_select_np(acc, fixed_delta):
+    """baselines.cpp:43-46 -> select_indices over [0, n) (selector.cpp:35-42):
+    ascending {j : |acc[j]| >= delta}, compared in fp64."""
+    return np.flatnonzero(np.abs(acc.astype(np.float64)) >= fixed_delta).astype(np.int64)
+
+
+def ref_topk_select(acc, k):
+    """The unmodified reference's topk_select on fp64 acc."""
+    a = np.ascontiguousarray(acc, dtype=np.float64)
+    out = np.zeros(max(k, 1), np.int64)
+    rc = ref().ref_topk_select(_ptr(a, C.c_double), a.shape[0], k, _ptr(out, C.c_int64))
+    if rc:
+        raise CheckError(rc, ref().ref_last_error().decode())
+    return out[:k]
+
+
+def ref_hard_threshold_select(acc, fixed_delta):
+    a = np.ascontiguousarray(acc, dtype=np.float64)
+    out = np.zeros(max(a.shape[0], 1), np.int64)
+    cnt = C.c_int64()
+    ref().ref_hard_threshold_select(_ptr(a, C.c_double), a.shape[0], fixed_delta,
+                                    _ptr(out, C.c_int64), C.byref(cnt))
+    return out[:cnt.value]
 
 
 class OracleEngine:

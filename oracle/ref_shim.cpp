@@ -21,6 +21,7 @@
 
 #include "exdyna.h"
 #include "sparsim/allocator.hpp"
+#include "sparsim/baselines.hpp"
 #include "sparsim/collectives.hpp"
 #include "sparsim/config.hpp"
 #include "sparsim/engine.hpp"
@@ -218,6 +219,26 @@ int ref_initial_threshold(const double* mags, int64_t m, double d, double* out) 
   } catch (const std::invalid_argument& e) {
     return fail(EXD_EINVAL, e.what());
   }
+}
+
+// topk_select (baselines.cpp:26-41): out gets k indices; returns 0 or EXD_EINVAL.
+int ref_topk_select(const double* acc, int64_t n, int64_t k, int64_t* out) {
+  try {
+    const auto idx = topk_select(std::span<const double>(acc, (size_t)n), k);
+    std::copy(idx.begin(), idx.end(), out);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(EXD_EINVAL, e.what());
+  }
+}
+
+// hard_threshold_select (baselines.cpp:43-46): out needs n slots; *count set.
+int ref_hard_threshold_select(const double* acc, int64_t n, double delta, int64_t* out,
+                              int64_t* count) {
+  const auto idx = hard_threshold_select(std::span<const double>(acc, (size_t)n), delta);
+  std::copy(idx.begin(), idx.end(), out);
+  *count = (int64_t)idx.size();
+  return 0;
 }
 
 // all_gather over n index lists given as (concatenated, counts).

@@ -67,6 +67,10 @@ def lib():
     _sig(L, "exd_gather_stats_of", C.c_int, [PI64, C.c_int32, C.POINTER(A.exd_gather_stats)])
     _sig(L, "exd_initial_threshold_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_double,
                                                       C.POINTER(C.c_double)])
+    _sig(L, "exd_topk_select_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_int64, P,
+                                                C.c_int64, P])
+    _sig(L, "exd_hard_threshold_select_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_double,
+                                                          P, C.c_int64, PI64, P])
     _sig(L, "exd_synthetic_gradient", C.c_int, [C.POINTER(A.exd_stream_spec), C.c_int64,
                                                 C.c_int32, C.c_int32, P, P])
     _sig(L, "exd_engine_create", C.c_int, [C.POINTER(A.exd_config), C.POINTER(A.exd_options),
@@ -119,6 +123,7 @@ EXPORTED = [
     "exd_build_topology", "exd_partition_range", "exd_rotate_to_partition_order",
     "exd_adjust_topology", "exd_allocate_partition", "exd_scale_threshold",
     "exd_gather_stats_of", "exd_initial_threshold_device", "exd_synthetic_gradient",
+    "exd_topk_select_device", "exd_hard_threshold_select_device",
     "exd_engine_create", "exd_nccl_unique_id", "exd_engine_create_rank", "exd_engine_destroy",
     "exd_engine_local_workers", "exd_engine_first_rank", "exd_engine_iteration",
     "exd_engine_sync_mode",

@@ -1,0 +1,260 @@
+// Baseline sparsifiers of the reference on the device:
+//   topk_select            baselines.cpp:26-41  (exact top-k by |acc|, ascending
+//                                                indices, ties toward the lower index)
+//   hard_threshold_select  baselines.cpp:43-46  (|acc| >= fixed_delta over [0, n_g))
+//
+// Both are one ordered stream compaction over the full vector, HBM-bound:
+//   count  per 4096-element tile: #strict (|a| above the cut) and #tie (|a| at it)
+//   scan   one CTA: exclusive tile offsets and the totals, need = k - #strict
+//   emit   per tile: re-read, block scan of packed {strict, tie} thread counts,
+//          element j is kept when strict, or tie with fewer than `need` ties
+//          before it; it lands at (#strict before j) + min(#tie before j, need)
+// Top-k first finds the cut, the k-th largest |acc|, with the K8 radix select
+// (launch_quantile, ascending position n_g - k). Hard threshold has no tie
+// class: strict = (double)|a| >= delta, the reference's comparison in fp64.
+// Algorithmic bytes: 2 reads of acc (count + emit) + 4 B per kept index
+// (+ 4 or 8 radix passes over acc for top-k).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "exdyna.h"
+#include "internal.cuh"
+
+namespace exd {
+namespace {
+
+constexpr int kBlThreads = 256;
+constexpr int kBlPer = 16;  // elements per thread per tile (contiguous)
+constexpr int kBlTile = kBlThreads * kBlPer;
+
+template <typename T> struct AbsBits;
+template <> struct AbsBits<float> {
+  __device__ static unsigned long long of(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+};
+template <> struct AbsBits<double> {
+  __device__ static unsigned long long of(double v) {
+    return (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+  }
+};
+
+struct Cut {
+  int topk;                  // 1: strict = bits > cut, tie = bits == cut; 0: |a| >= delta
+  double delta;
+  const void* cut_bits;      // device: |value| bits of the k-th largest (top-k)
+};
+
+// packed {strict (low 16 bits), tie (high 16 bits)} counts of one thread's run
+template <typename T>
+__device__ __forceinline__ uint32_t classify(const T* acc, int64_t n_g, int64_t base, const Cut& c,
+                                             unsigned long long cut, uint32_t* flags) {
+  // the run is 64 B (f32) or 128 B (f64) aligned: 128-bit loads when whole
+  T r[kBlPer];
+  if (base + kBlPer <= n_g) {
+    const int4* p = reinterpret_cast<const int4*>(acc + base);
+#pragma unroll
+    for (int i = 0; i < kBlPer * (int)sizeof(T) / 16; ++i)
+      reinterpret_cast<int4*>(r)[i] = __ldg(p + i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kBlPer; ++i) r[i] = base + i < n_g ? acc[base + i] : (T)0;
+  }
+  uint32_t packed = 0, f = 0;
+#pragma unroll
+  for (int i = 0; i < kBlPer; ++i) {
+    const int64_t j = base + i;
+    if (j < n_g) {
+      const T v = r[i];
+      uint32_t s, t;
+      if (c.topk) {
+        const unsigned long long b = AbsBits<T>::of(v);
+        s = b > cut;
+        t = b == cut;
+      } else {
+        s = (double)(v < (T)0 ? -v : v) >= c.delta;
+        t = 0;
+      }
+      f |= (s | (t << 1)) << (2 * i);
+      packed += s + (t << 16);
+    }
+  }
+  *flags = f;
+  return packed;
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned long long load_cut(const Cut& c) {
+  if (!c.topk) return 0;
+  if (sizeof(T) == 4) return *static_cast<const uint32_t*>(c.cut_bits);
+  return *static_cast<const unsigned long long*>(c.cut_bits);
+}
+
+// block-wide exclusive scan of one packed word per thread; *total gets the sum
+__device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t warp_sum[kBlThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < kBlThreads / 32 ? warp_sum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < kBlThreads / 32) warp_sum[lane] = s;
+  }
+  __syncthreads();
+  const uint32_t before = (w ? warp_sum[w - 1] : 0) + x - v;
+  *total = warp_sum[kBlThreads / 32 - 1];
+  return before;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlThreads) bl_count_kernel(const T* __restrict__ acc, int64_t n_g,
+                                                             Cut c, uint32_t* tile_counts) {
+  const unsigned long long cut = load_cut<T>(c);
+  const int64_t base = (int64_t)blockIdx.x * kBlTile + (int64_t)threadIdx.x * kBlPer;
+  uint32_t f;
+  uint32_t mine = classify<T>(acc, n_g, base, c, cut, &f);
+  uint32_t total;
+  block_exclusive(mine, &total);
+  if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
+}
+
+// totals[0] = #strict, totals[1] = #tie, totals[2] = need (ties kept)
+__global__ void __launch_bounds__(1024) bl_scan_kernel(const uint32_t* tile_counts, int64_t tiles,
+                                                       int64_t k, int topk, int64_t* offs_strict,
+                                                       int64_t* offs_tie, int64_t* totals) {
+  __shared__ long long ws[32], wt[32];
+  __shared__ long long carry_s, carry_t;
+  if (threadIdx.x == 0) carry_s = carry_t = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t b = 0; b < tiles; b += 1024) {
+    const int64_t i = b + threadIdx.x;
+    const uint32_t p = i < tiles ? tile_counts[i] : 0;
+    long long s = p & 0xffffu, t = p >> 16, xs = s, xt = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long ys = __shfl_up_sync(0xffffffffu, xs, o);
+      const long long yt = __shfl_up_sync(0xffffffffu, xt, o);
+      if (lane >= o) { xs += ys; xt += yt; }
+    }
+    if (lane == 31) { ws[w] = xs; wt[w] = xt; }
+    __syncthreads();
+    if (w == 0) {
+      long long a = ws[lane], bt = wt[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long ya = __shfl_up_sync(0xffffffffu, a, o);
+        const long long yb = __shfl_up_sync(0xffffffffu, bt, o);
+        if (lane >= o) { a += ya; bt += yb; }
+      }
+      ws[lane] = a;
+      wt[lane] = bt;
+    }
+    __syncthreads();
+    const long long ps = carry_s + (w ? ws[w - 1] : 0) + xs - s;
+    const long long pt = carry_t + (w ? wt[w - 1] : 0) + xt - t;
+    if (i < tiles) {
+      offs_strict[i] = ps;
+      offs_tie[i] = pt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry_s += ws[31];
+      carry_t += wt[31];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    totals[0] = carry_s;
+    totals[1] = carry_t;
+    long long need = topk ? k - carry_s : 0;
+    if (need < 0) need = 0;
+    if (need > carry_t) need = carry_t;
+    totals[2] = need;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlThreads) bl_emit_kernel(const T* __restrict__ acc, int64_t n_g,
+                                                            Cut c, const int64_t* offs_strict,
+                                                            const int64_t* offs_tie,
+                                                            const int64_t* totals, int32_t* out,
+                                                            int64_t cap) {
+  const unsigned long long cut = load_cut<T>(c);
+  const int64_t base = (int64_t)blockIdx.x * kBlTile + (int64_t)threadIdx.x * kBlPer;
+  uint32_t f;
+  const uint32_t mine = classify<T>(acc, n_g, base, c, cut, &f);
+  uint32_t total;
+  const uint32_t before = block_exclusive(mine, &total);
+  if (mine == 0) return;
+  const long long need = totals[2];
+  long long s = offs_strict[blockIdx.x] + (before & 0xffffu);
+  long long t = offs_tie[blockIdx.x] + (before >> 16);
+#pragma unroll
+  for (int i = 0; i < kBlPer; ++i) {
+    const uint32_t fi = (f >> (2 * i)) & 3u;
+    long long pos = -1;
+    if (fi & 1u) {
+      pos = s + (t < need ? t : need);
+      ++s;
+    } else if (fi & 2u) {
+      if (t < need) pos = s + t;
+      ++t;
+    }
+    if (pos >= 0 && pos < cap) out[pos] = (int32_t)(base + i);
+  }
+}
+
+template <typename T>
+cudaError_t baseline_select_t(const T* acc, int64_t n_g, const Cut& c, int64_t k, int32_t* out,
+                              int64_t cap, int64_t* totals_dev, void* scratch, cudaStream_t s) {
+  const int64_t tiles = (n_g + kBlTile - 1) / kBlTile;
+  uint32_t* tile_counts = static_cast<uint32_t*>(scratch);
+  int64_t* offs_strict = reinterpret_cast<int64_t*>(
+      static_cast<char*>(scratch) + ((tiles * 4 + 15) / 16) * 16);
+  int64_t* offs_tie = offs_strict + tiles;
+  bl_count_kernel<T><<<(unsigned)tiles, kBlThreads, 0, s>>>(acc, n_g, c, tile_counts);
+  bl_scan_kernel<<<1, 1024, 0, s>>>(tile_counts, tiles, k, c.topk, offs_strict, offs_tie,
+                                    totals_dev);
+  bl_emit_kernel<T><<<(unsigned)tiles, kBlThreads, 0, s>>>(acc, n_g, c, offs_strict, offs_tie,
+                                                          totals_dev, out, cap);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t baseline_scratch_bytes(int64_t n_g) {
+  const int64_t tiles = (n_g + kBlTile - 1) / kBlTile;
+  return (size_t)(((tiles * 4 + 15) / 16) * 16 + tiles * 16) + quantile_scratch_bytes() + 64;
+}
+
+// topk: cut = |acc| at ascending position n_g - k (the k-th largest);
+// otherwise |acc| >= delta. scratch: baseline_scratch_bytes(n_g) device bytes;
+// totals_dev: 3 int64 {#strict, #tie, ties kept}.
+cudaError_t launch_baseline_select(const void* acc, int64_t n_g, int dtype, int topk, int64_t k,
+                                   double delta, int32_t* out, int64_t cap, int64_t* totals_dev,
+                                   void* scratch, cudaStream_t s) {
+  Cut c{topk, delta, nullptr};
+  char* base = static_cast<char*>(scratch);
+  char* qscratch = base + (baseline_scratch_bytes(n_g) - quantile_scratch_bytes() - 64);
+  char* cut_bits = qscratch + quantile_scratch_bytes();
+  if (topk) {
+    cudaError_t e = launch_quantile(acc, n_g, n_g - k, dtype, qscratch, cut_bits, s);
+    if (e != cudaSuccess) return e;
+    c.cut_bits = cut_bits;
+  }
+  return dtype == EXD_F64
+             ? baseline_select_t<double>(static_cast<const double*>(acc), n_g, c, k, out, cap,
+                                         totals_dev, scratch, s)
+             : baseline_select_t<float>(static_cast<const float*>(acc), n_g, c, k, out, cap,
+                                        totals_dev, scratch, s);
+}
+
+}  // namespace exd

@@ -1145,6 +1145,54 @@ int exd_initial_threshold_device(const void* mags_dev, int64_t m, int32_t dtype,
   return EXD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// topk_select / hard_threshold_select (baselines.cpp:26-46) on the device
+int baseline_select(const void* acc, int64_t n_g, int32_t dtype, int topk, int64_t k,
+                    double delta, int32_t* idx, int64_t cap, int64_t* count, void* stream) {
+  if (dtype != EXD_F32 && dtype != EXD_F64) return set_err(EXD_EINVAL, "dtype out of range");
+  if (n_g < 0 || n_g > 0x7fffffffLL) return set_err(EXD_EINVAL, "n_g out of range");
+  if (topk && (k < 1 || k > n_g)) return set_err(EXD_EINVAL, "topk_select: k out of range");
+  if (n_g == 0) {
+    if (count) *count = 0;
+    return EXD_OK;
+  }
+  if (!acc || (!idx && cap > 0)) return set_err(EXD_EINVAL, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void* scratch = nullptr;
+  const size_t sb = baseline_scratch_bytes(n_g) + 3 * sizeof(int64_t);
+  CU(cudaMallocAsync(&scratch, sb, s));
+  int64_t* totals = reinterpret_cast<int64_t*>(static_cast<char*>(scratch) + sb - 3 * sizeof(int64_t));
+  cudaError_t e = launch_baseline_select(acc, n_g, dtype, topk, k, delta, idx, cap, totals,
+                                         scratch, s);
+  int64_t host[3] = {0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host, totals, sizeof(host), cudaMemcpyDeviceToHost, s);
+  cudaError_t f = cudaFreeAsync(scratch, s);
+  if (e == cudaSuccess) e = f;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(EXD_ECUDA, std::string("baseline select: ") + cudaGetErrorString(e));
+  const int64_t n_sel = host[0] + host[2];
+  if (topk && n_sel != k) return set_err(EXD_EINVARIANT, "topk_select: selected count != k");
+  if (count) *count = n_sel;
+  return EXD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int exd_topk_select_device(const void* acc_dev, int64_t n_g, int32_t dtype, int64_t k,
+                           int32_t* idx_dev, int64_t cap, void* cuda_stream) {
+  if (cap < k) return set_err(EXD_EINVAL, "topk_select: output capacity below k");
+  return baseline_select(acc_dev, n_g, dtype, 1, k, 0.0, idx_dev, cap, nullptr, cuda_stream);
+}
+
+int exd_hard_threshold_select_device(const void* acc_dev, int64_t n_g, int32_t dtype,
+                                     double fixed_delta, int32_t* idx_dev, int64_t cap,
+                                     int64_t* count, void* cuda_stream) {
+  return baseline_select(acc_dev, n_g, dtype, 0, 0, fixed_delta, idx_dev, cap, count, cuda_stream);
+}
+
 int exd_synthetic_gradient(const exd_stream_spec* spec, int64_t t, int32_t rank, int32_t dtype,
                            void* out_dev, void* cuda_stream) {
   if (!spec || spec->nseg < 1 || spec->nseg > EXD_MAX_SEGMENTS)

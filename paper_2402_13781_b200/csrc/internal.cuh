@@ -245,6 +245,11 @@ cudaError_t launch_conservation(const int32_t* uni, const CountRec* counts, int 
                                 uint32_t* bitmap, uint32_t* flag, RunConst rc, cudaStream_t s);
 cudaError_t launch_p2p_sync(const P2PArgs& a, RunConst rc, cudaStream_t s);
 cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s);
+// baseline sparsifiers (baselines.cpp:26-46), baselines.cu
+size_t baseline_scratch_bytes(int64_t n_g);
+cudaError_t launch_baseline_select(const void* acc, int64_t n_g, int dtype, int topk, int64_t k,
+                                   double delta, int32_t* out, int64_t cap, int64_t* totals_dev,
+                                   void* scratch, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
 

@@ -11,6 +11,7 @@ the B200 library through the C ABI of include/exdyna.h:
     gather_stats                         collectives.cpp:22-45 (accounting)
     Engine(cfg, opt).step() -> IterationRecord   engine.hpp:61-105, engine.cpp:274-350
     SyntheticStream                      workloads.hpp:89-99 (generated on device)
+    topk_select / hard_threshold_select  baselines.hpp:25-34, baselines.cpp:26-46 (device)
 
 std::invalid_argument maps to InvalidArgument (a ValueError) and
 sparsim::EngineError to EngineError. Device pointers are plain integers
@@ -32,7 +33,7 @@ __all__ = [
     "initial_threshold_device", "GatherStats", "gather_stats", "EngineOptions",
     "IterationRecord", "Engine", "StreamSpec", "SyntheticStream", "InvalidArgument",
     "EngineError", "DeviceError", "Unsupported", "nccl_unique_id", "flush_l2", "format_csv",
-    "summarize",
+    "summarize", "topk_select", "hard_threshold_select",
 ]
 
 
@@ -183,6 +184,46 @@ def initial_threshold_device(mags_ptr: int, m: int, d: float, dtype: str = "f32"
     check(lib().exd_initial_threshold_device(C.c_void_p(mags_ptr), m, _dtype_code(dtype), d,
                                              C.byref(out)))
     return out.value
+
+
+def _acc_args(acc):
+    """(device pointer, n_g, dtype code) of a contiguous CUDA fp32/fp64 tensor."""
+    import torch
+    if not (isinstance(acc, torch.Tensor) and acc.is_cuda and acc.dim() == 1
+            and acc.is_contiguous() and acc.dtype in (torch.float32, torch.float64)):
+        raise InvalidArgument("acc must be a contiguous 1-D CUDA float32/float64 tensor")
+    code = A.EXD_F64 if acc.dtype == torch.float64 else A.EXD_F32
+    return acc.data_ptr(), acc.numel(), code
+
+
+def _stream_of(acc):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(acc.device).cuda_stream)
+
+
+def topk_select(acc, k: int):
+    """baselines.cpp:26-41: the k indices of largest |acc| (ties toward the
+    lower index), ascending, as a device int32 tensor. Raises InvalidArgument
+    ("topk_select: k out of range") unless 1 <= k <= acc.numel()."""
+    import torch
+    ptr, n_g, code = _acc_args(acc)
+    out = torch.empty(max(k, 0), dtype=torch.int32, device=acc.device)
+    check(lib().exd_topk_select_device(C.c_void_p(ptr), n_g, code, k, C.c_void_p(out.data_ptr()),
+                                       out.numel(), _stream_of(acc)))
+    return out
+
+
+def hard_threshold_select(acc, fixed_delta: float):
+    """baselines.cpp:43-46: ascending {j : |acc[j]| >= fixed_delta} over the
+    whole vector (compared in fp64), as a device int32 tensor."""
+    import torch
+    ptr, n_g, code = _acc_args(acc)
+    out = torch.empty(n_g, dtype=torch.int32, device=acc.device)
+    cnt = C.c_int64()
+    check(lib().exd_hard_threshold_select_device(C.c_void_p(ptr), n_g, code, float(fixed_delta),
+                                                 C.c_void_p(out.data_ptr()), out.numel(),
+                                                 C.byref(cnt), _stream_of(acc)))
+    return out[:cnt.value]
 
 
 @dataclass
