@@ -8,12 +8,17 @@
 //   sparsim::Engine            -> exdyna::Engine             (engine.hpp:61-105)
 //   sparsim::IterationRecord   -> exdyna::IterationRecord    (types.hpp:84-103)
 //   sparsim::EngineError       -> exdyna::EngineError        (engine.hpp:47-50)
+//   sparsim::topk_select /
+//   sparsim::hard_threshold_select -> exdyna::topk_select /
+//                                 exdyna::hard_threshold_select (baselines.hpp:25-34)
 //
 // Differences a caller sees: gradients are DEVICE buffers (one per local
 // worker) instead of a host GradientSource callback (step_host() takes the
 // host buffers such a source fills); the engine works in fp32
 // (Precision::F32) or in the reference's fp64 (Precision::F64).
 #pragma once
+
+#include <cuda_runtime.h>
 
 #include <cstring>
 #include <optional>
@@ -103,6 +108,16 @@ inline PartitionTopology build_topology(int64_t n_g, int64_t n_b, int n, int64_t
 }
 
 enum class Precision { F32 = EXD_F32, F64 = EXD_F64 };
+
+// baselines.hpp:25-34 over a DEVICE vector acc (n_g elements of `precision`);
+// the indices come back to the host in ascending order, like the reference's
+// std::vector<Index>. `idx_dev` is caller scratch of at least k (top-k) or
+// n_g (hard threshold) int32; `stream` is a cudaStream_t (nullptr: default).
+inline std::vector<int64_t> topk_select(const void* acc_dev, int64_t n_g, Precision precision,
+                                        int64_t k, int32_t* idx_dev, void* stream = nullptr);
+inline std::vector<int64_t> hard_threshold_select(const void* acc_dev, int64_t n_g,
+                                                  Precision precision, double fixed_delta,
+                                                  int32_t* idx_dev, void* stream = nullptr);
 
 struct EngineOptions {
   bool static_partitions = false;
@@ -235,5 +250,32 @@ class Engine {
   EngineOptions opt_;
   exd_engine* h_ = nullptr;
 };
+
+namespace detail {
+inline std::vector<int64_t> copy_indices(const int32_t* idx_dev, int64_t count) {
+  std::vector<int32_t> h(static_cast<size_t>(count));
+  if (count > 0 &&
+      cudaMemcpy(h.data(), idx_dev, h.size() * sizeof(int32_t), cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+    throw DeviceError("copy of selected indices failed");
+  return std::vector<int64_t>(h.begin(), h.end());
+}
+}  // namespace detail
+
+inline std::vector<int64_t> topk_select(const void* acc_dev, int64_t n_g, Precision precision,
+                                        int64_t k, int32_t* idx_dev, void* stream) {
+  check(exd_topk_select_device(acc_dev, n_g, static_cast<int32_t>(precision), k, idx_dev,
+                               k, stream));
+  return detail::copy_indices(idx_dev, k);
+}
+
+inline std::vector<int64_t> hard_threshold_select(const void* acc_dev, int64_t n_g,
+                                                  Precision precision, double fixed_delta,
+                                                  int32_t* idx_dev, void* stream) {
+  int64_t count = 0;
+  check(exd_hard_threshold_select_device(acc_dev, n_g, static_cast<int32_t>(precision),
+                                         fixed_delta, idx_dev, n_g, &count, stream));
+  return detail::copy_indices(idx_dev, count);
+}
 
 }  // namespace exdyna

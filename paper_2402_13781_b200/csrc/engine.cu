@@ -1160,16 +1160,38 @@ int baseline_select(const void* acc, int64_t n_g, int32_t dtype, int topk, int64
   }
   if (!acc || (!idx && cap > 0)) return set_err(EXD_EINVAL, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  void* scratch = nullptr;
+  // Grow-only scratch per device, plus a pinned read-back slot; the call is
+  // synchronous, so one caller at a time holds them.
+  struct Scratch {
+    void* dev = nullptr;
+    size_t bytes = 0;
+    int64_t* host = nullptr;
+  };
+  static std::mutex mu;
+  static Scratch cache[64];
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return set_err(EXD_EINVAL, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  Scratch& sc = cache[dev];
   const size_t sb = baseline_scratch_bytes(n_g) + 3 * sizeof(int64_t);
-  CU(cudaMallocAsync(&scratch, sb, s));
+  if (sc.bytes < sb) {
+    if (sc.dev) {
+      CU(cudaStreamSynchronize(s));
+      CU(cudaFree(sc.dev));
+      sc.dev = nullptr;
+      sc.bytes = 0;
+    }
+    CU(cudaMalloc(&sc.dev, sb));
+    sc.bytes = sb;
+  }
+  if (!sc.host) CU(cudaMallocHost(&sc.host, 3 * sizeof(int64_t)));
+  void* scratch = sc.dev;
   int64_t* totals = reinterpret_cast<int64_t*>(static_cast<char*>(scratch) + sb - 3 * sizeof(int64_t));
   cudaError_t e = launch_baseline_select(acc, n_g, dtype, topk, k, delta, idx, cap, totals,
                                          scratch, s);
-  int64_t host[3] = {0, 0, 0};
-  if (e == cudaSuccess) e = cudaMemcpyAsync(host, totals, sizeof(host), cudaMemcpyDeviceToHost, s);
-  cudaError_t f = cudaFreeAsync(scratch, s);
-  if (e == cudaSuccess) e = f;
+  int64_t* host = sc.host;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host, totals, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_err(EXD_ECUDA, std::string("baseline select: ") + cudaGetErrorString(e));
   const int64_t n_sel = host[0] + host[2];

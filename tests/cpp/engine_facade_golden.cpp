@@ -83,5 +83,34 @@ int main() {
   cudaFree(d0);
   cudaFree(d1);
   std::printf("engine_facade_golden: PASS\n");
+  // baselines through the facade: test_baselines.cpp:27-37, 66-71 known answers
+  {
+    const std::vector<double> a{0.1, -0.5, 0.3}, b{0.5, 0.5, 0.1}, c{0.1, 0.4};
+    double* dv;
+    int32_t* di;
+    cudaMalloc(&dv, 3 * sizeof(double));
+    cudaMalloc(&di, 3 * sizeof(int32_t));
+    const auto F64 = exdyna::Precision::F64;
+    cudaMemcpy(dv, a.data(), 3 * sizeof(double), cudaMemcpyHostToDevice);
+    EXPECT((exdyna::topk_select(dv, 3, F64, 2, di) == std::vector<int64_t>{1, 2}));
+    EXPECT((exdyna::topk_select(dv, 3, F64, 3, di) == std::vector<int64_t>{0, 1, 2}));
+    cudaMemcpy(dv, b.data(), 3 * sizeof(double), cudaMemcpyHostToDevice);
+    EXPECT((exdyna::topk_select(dv, 3, F64, 1, di) == std::vector<int64_t>{0}));
+    EXPECT((exdyna::topk_select(dv, 3, F64, 2, di) == std::vector<int64_t>{0, 1}));
+    bool threw = false;
+    try {
+      exdyna::topk_select(dv, 3, F64, 4, di);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    cudaMemcpy(dv, c.data(), 2 * sizeof(double), cudaMemcpyHostToDevice);
+    EXPECT((exdyna::hard_threshold_select(dv, 2, F64, 0.3, di) == std::vector<int64_t>{1}));
+    EXPECT((exdyna::hard_threshold_select(dv, 2, F64, 0.05, di) == std::vector<int64_t>{0, 1}));
+    EXPECT(exdyna::hard_threshold_select(dv, 2, F64, 9.0, di).empty());
+    cudaFree(dv);
+    cudaFree(di);
+  }
+  std::printf("PASS baselines\n");
   return 0;
 }
