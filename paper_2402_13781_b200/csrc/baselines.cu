@@ -188,15 +188,17 @@ __global__ void __launch_bounds__(kBlThreads) bl_emit_kernel(const T* __restrict
                                                             const int64_t* totals, int32_t* out,
                                                             int64_t cap) {
   const unsigned long long cut = load_cut<T>(c);
+  // the tile's offsets are loaded with the data, not after the block scan
+  const long long need = totals[2];
+  const long long s0 = offs_strict[blockIdx.x], t0 = offs_tie[blockIdx.x];
   const int64_t base = (int64_t)blockIdx.x * kBlTile + (int64_t)threadIdx.x * kBlPer;
   uint32_t f;
   const uint32_t mine = classify<T>(acc, n_g, base, c, cut, &f);
   uint32_t total;
   const uint32_t before = block_exclusive(mine, &total);
   if (mine == 0) return;
-  const long long need = totals[2];
-  long long s = offs_strict[blockIdx.x] + (before & 0xffffu);
-  long long t = offs_tie[blockIdx.x] + (before >> 16);
+  long long s = s0 + (before & 0xffffu);
+  long long t = t0 + (before >> 16);
 #pragma unroll
   for (int i = 0; i < kBlPer; ++i) {
     const uint32_t fi = (f >> (2 * i)) & 3u;

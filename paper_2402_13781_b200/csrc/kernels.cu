@@ -1838,18 +1838,28 @@ __global__ void __launch_bounds__(256) quantile_hist_kernel(const T* v, int64_t 
   if (h[threadIdx.x]) atomicAdd(&q->hist[threadIdx.x], h[threadIdx.x]);
 }
 
-__global__ void quantile_pick_kernel(QState* q, int shift) {
-  if (threadIdx.x != 0) return;
-  long long r = q->rank;
-  int d = 0;
-  for (; d < 256; ++d) {
-    if (r < (long long)q->hist[d]) break;
-    r -= q->hist[d];
+// One thread per digit: inclusive scan of the 256 bins in shared memory; the
+// digit whose [exclusive, inclusive) count range holds rank is the next digit.
+__global__ void __launch_bounds__(256) quantile_pick_kernel(QState* q, int shift) {
+  __shared__ long long inc[256];
+  const int i = threadIdx.x;
+  const long long r = q->rank;
+  const long long v = q->hist[i];
+  q->hist[i] = 0;  // each thread clears the bin it has read
+  inc[i] = v;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const long long add = i >= o ? inc[i - o] : 0;
+    __syncthreads();
+    inc[i] += add;
+    __syncthreads();
   }
-  q->rank = r;
-  q->prefix |= (unsigned long long)d << shift;
-  q->mask |= 0xffULL << shift;
-  for (int i = 0; i < 256; ++i) q->hist[i] = 0;
+  const long long excl = inc[i] - v;
+  if (v > 0 && r >= excl && r < inc[i]) {
+    q->rank = r - excl;
+    q->prefix |= (unsigned long long)i << shift;
+    q->mask |= 0xffULL << shift;
+  }
 }
 
 template <typename T>
@@ -1883,7 +1893,7 @@ cudaError_t quantile_t(const T* v, int64_t m, int64_t pos, QState* q, T* out, cu
   if (blocks < 1) blocks = 1;
   for (int shift = Bits<T>::W - 8; shift >= 0; shift -= 8) {
     quantile_hist_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(v, m, q, shift);
-    quantile_pick_kernel<<<1, 32, 0, s>>>(q, shift);
+    quantile_pick_kernel<<<1, 256, 0, s>>>(q, shift);
   }
   quantile_out_kernel<T><<<1, 32, 0, s>>>(q, out);
   return cudaGetLastError();
