@@ -4,7 +4,7 @@
 //   hard_threshold_select  baselines.cpp:43-46  (|acc| >= fixed_delta over [0, n_g))
 //
 // Both are one ordered stream compaction over the full vector, HBM-bound:
-//   count  per 4096-element tile: #strict (|a| above the cut) and #tie (|a| at it)
+//   count  per tile (8192 f32 / 4096 f64 elements): #strict (|a| above the cut) and #tie (|a| at it)
 //   scan   one CTA: exclusive tile offsets and the totals, need = k - #strict
 //   emit   per tile: re-read, block scan of packed {strict, tie} thread counts,
 //          element j is kept when strict, or tie with fewer than `need` ties
@@ -24,8 +24,8 @@ namespace exd {
 namespace {
 
 constexpr int kBlThreads = 256;
-constexpr int kBlPer = 16;  // elements per thread per tile (contiguous)
-constexpr int kBlTile = kBlThreads * kBlPer;
+constexpr int kBlSlots = 8;  // 128-bit slots per thread per tile (128 B in flight per thread)
+constexpr int kBlTileMin = kBlThreads * kBlSlots * 2;  // elements per tile, f64 (f32: 2x)
 
 template <typename T> struct AbsBits;
 template <> struct AbsBits<float> {
@@ -43,42 +43,65 @@ struct Cut {
   const void* cut_bits;      // device: |value| bits of the k-th largest (top-k)
 };
 
-// packed {strict (low 16 bits), tie (high 16 bits)} counts of one thread's run
+// Layout of one tile: warp w owns the contiguous 32*PER elements (1024 f32 /
+// 512 f64); inside it, 128-bit slot i of lane l holds elements
+// i*(32*V) + l*V + [0, V) (V = 4 f32 / 2 f64), so every load instruction of a
+// warp reads 512 contiguous bytes. Index order inside a warp chunk is
+// (slot, lane, component).
+template <typename T> struct Lay {
+  static constexpr int V = 16 / (int)sizeof(T);   // elements per 128-bit slot
+  static constexpr int S = kBlSlots;              // slots per thread
+  static constexpr int PER = S * V;               // elements per thread
+  static constexpr int TILE = kBlThreads * PER;   // 8192 f32 / 4096 f64
+};
+
+// per-slot packed {strict (low 16 bits), tie (high 16 bits)} counts; flags
+// hold 2 bits per element (bit 0 strict, bit 1 tie) in (slot, component) order
 template <typename T>
-__device__ __forceinline__ uint32_t classify(const T* acc, int64_t n_g, int64_t base, const Cut& c,
-                                             unsigned long long cut, uint32_t* flags) {
-  // the run is 64 B (f32) or 128 B (f64) aligned: 128-bit loads when whole
-  T r[kBlPer];
-  if (base + kBlPer <= n_g) {
-    const int4* p = reinterpret_cast<const int4*>(acc + base);
+__device__ __forceinline__ void classify(const T* acc, int64_t n_g, int64_t wbase, const Cut& c,
+                                         unsigned long long cut, uint32_t (&pc)[Lay<T>::S],
+                                         unsigned long long* flags) {
+  constexpr int V = Lay<T>::V, S = Lay<T>::S;
+  const int lane = threadIdx.x & 31;
+  T r[Lay<T>::PER];
+  if (wbase + 32 * Lay<T>::PER <= n_g) {
+    const int4* p = reinterpret_cast<const int4*>(acc + wbase) + lane;
 #pragma unroll
-    for (int i = 0; i < kBlPer * (int)sizeof(T) / 16; ++i)
-      reinterpret_cast<int4*>(r)[i] = __ldg(p + i);
+    for (int i = 0; i < S; ++i) reinterpret_cast<int4*>(r)[i] = __ldg(p + 32 * i);
   } else {
 #pragma unroll
-    for (int i = 0; i < kBlPer; ++i) r[i] = base + i < n_g ? acc[base + i] : (T)0;
-  }
-  uint32_t packed = 0, f = 0;
+    for (int i = 0; i < S; ++i)
 #pragma unroll
-  for (int i = 0; i < kBlPer; ++i) {
-    const int64_t j = base + i;
-    if (j < n_g) {
-      const T v = r[i];
-      uint32_t s, t;
-      if (c.topk) {
-        const unsigned long long b = AbsBits<T>::of(v);
-        s = b > cut;
-        t = b == cut;
-      } else {
-        s = (double)(v < (T)0 ? -v : v) >= c.delta;
-        t = 0;
+      for (int q = 0; q < V; ++q) {
+        const int64_t j = wbase + i * 32 * V + lane * V + q;
+        r[i * V + q] = j < n_g ? acc[j] : (T)0;
       }
-      f |= (s | (t << 1)) << (2 * i);
-      packed += s + (t << 16);
+  }
+  unsigned long long f = 0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int64_t j = wbase + i * 32 * V + lane * V + q;
+      if (j < n_g) {
+        const T v = r[i * V + q];
+        uint32_t st, ti;
+        if (c.topk) {
+          const unsigned long long b = AbsBits<T>::of(v);
+          st = b > cut;
+          ti = b == cut;
+        } else {
+          st = (double)(v < (T)0 ? -v : v) >= c.delta;
+          ti = 0;
+        }
+        f |= (unsigned long long)(st | (ti << 1)) << (2 * (i * V + q));
+        packed += st + (ti << 16);
+      }
     }
+    pc[i] = packed;
   }
   *flags = f;
-  return packed;
 }
 
 template <typename T>
@@ -119,9 +142,13 @@ template <typename T>
 __global__ void __launch_bounds__(kBlThreads) bl_count_kernel(const T* __restrict__ acc, int64_t n_g,
                                                              Cut c, uint32_t* tile_counts) {
   const unsigned long long cut = load_cut<T>(c);
-  const int64_t base = (int64_t)blockIdx.x * kBlTile + (int64_t)threadIdx.x * kBlPer;
-  uint32_t f;
-  uint32_t mine = classify<T>(acc, n_g, base, c, cut, &f);
+  const int64_t wbase = (int64_t)blockIdx.x * Lay<T>::TILE + (int64_t)(threadIdx.x >> 5) * 32 * Lay<T>::PER;
+  unsigned long long f;
+  uint32_t pc[Lay<T>::S];
+  classify<T>(acc, n_g, wbase, c, cut, pc, &f);
+  uint32_t mine = 0;
+#pragma unroll
+  for (int i = 0; i < Lay<T>::S; ++i) mine += pc[i];
   uint32_t total;
   block_exclusive(mine, &total);
   if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
@@ -187,37 +214,62 @@ __global__ void __launch_bounds__(kBlThreads) bl_emit_kernel(const T* __restrict
                                                             const int64_t* offs_tie,
                                                             const int64_t* totals, int32_t* out,
                                                             int64_t cap) {
+  constexpr int V = Lay<T>::V, S = Lay<T>::S;
   const unsigned long long cut = load_cut<T>(c);
-  // the tile's offsets are loaded with the data, not after the block scan
+  // the tile's offsets are loaded with the data, not after the scans
   const long long need = totals[2];
   const long long s0 = offs_strict[blockIdx.x], t0 = offs_tie[blockIdx.x];
-  const int64_t base = (int64_t)blockIdx.x * kBlTile + (int64_t)threadIdx.x * kBlPer;
-  uint32_t f;
-  const uint32_t mine = classify<T>(acc, n_g, base, c, cut, &f);
-  uint32_t total;
-  const uint32_t before = block_exclusive(mine, &total);
-  if (mine == 0) return;
-  long long s = s0 + (before & 0xffffu);
-  long long t = t0 + (before >> 16);
+  const int lane = threadIdx.x & 31;
+  const int64_t wbase = (int64_t)blockIdx.x * Lay<T>::TILE + (int64_t)(threadIdx.x >> 5) * 32 * Lay<T>::PER;
+  unsigned long long f;
+  uint32_t pc[S];
+  classify<T>(acc, n_g, wbase, c, cut, pc, &f);
+  // per slot: lane-exclusive prefix inside the warp and the slot's warp total
+  uint32_t excl[S], wsum = 0;
 #pragma unroll
-  for (int i = 0; i < kBlPer; ++i) {
-    const uint32_t fi = (f >> (2 * i)) & 3u;
-    long long pos = -1;
-    if (fi & 1u) {
-      pos = s + (t < need ? t : need);
-      ++s;
-    } else if (fi & 2u) {
-      if (t < need) pos = s + t;
-      ++t;
+  for (int i = 0; i < S; ++i) {
+    uint32_t x = pc[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if (pos >= 0 && pos < cap) out[pos] = (int32_t)(base + i);
+    excl[i] = wsum + x - pc[i];
+    wsum += __shfl_sync(0xffffffffu, x, 31);
+  }
+  // warps in order: lane 0 carries the warp's total into the block scan
+  uint32_t total;
+  const uint32_t wb = __shfl_sync(0xffffffffu, block_exclusive(lane == 0 ? wsum : 0u, &total), 0);
+  if (f == 0) return;
+  // walk only the set flag bits, in element order (bit 2q: strict, 2q+1: tie)
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    uint32_t sb = (uint32_t)(f >> (2 * i * V)) & ((1u << (2 * V)) - 1u);
+    if (sb == 0) continue;
+    const uint32_t before = wb + excl[i];
+    long long s = s0 + (before & 0xffffu);
+    long long t = t0 + (before >> 16);
+    const int64_t jbase = wbase + i * 32 * V + lane * V;
+    while (sb) {
+      const int b = __ffs(sb) - 1;
+      sb &= sb - 1;
+      long long pos = -1;
+      if (b & 1) {
+        if (t < need) pos = s + t;
+        ++t;
+      } else {
+        pos = s + (t < need ? t : need);
+        ++s;
+      }
+      if (pos >= 0 && pos < cap) out[pos] = (int32_t)(jbase + (b >> 1));
+    }
   }
 }
 
 template <typename T>
 cudaError_t baseline_select_t(const T* acc, int64_t n_g, const Cut& c, int64_t k, int32_t* out,
                               int64_t cap, int64_t* totals_dev, void* scratch, cudaStream_t s) {
-  const int64_t tiles = (n_g + kBlTile - 1) / kBlTile;
+  const int64_t tiles = (n_g + Lay<T>::TILE - 1) / Lay<T>::TILE;
   uint32_t* tile_counts = static_cast<uint32_t*>(scratch);
   int64_t* offs_strict = reinterpret_cast<int64_t*>(
       static_cast<char*>(scratch) + ((tiles * 4 + 15) / 16) * 16);
@@ -233,7 +285,7 @@ cudaError_t baseline_select_t(const T* acc, int64_t n_g, const Cut& c, int64_t k
 }  // namespace
 
 size_t baseline_scratch_bytes(int64_t n_g) {
-  const int64_t tiles = (n_g + kBlTile - 1) / kBlTile;
+  const int64_t tiles = (n_g + kBlTileMin - 1) / kBlTileMin;  // the f64 tiling is the finer
   return (size_t)(((tiles * 4 + 15) / 16) * 16 + tiles * 16) + quantile_scratch_bytes() + 64;
 }
 
