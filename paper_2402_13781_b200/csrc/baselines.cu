@@ -13,7 +13,7 @@
 // (launch_quantile, ascending position n_g - k). Hard threshold has no tie
 // class: strict = (double)|a| >= delta, the reference's comparison in fp64.
 // Algorithmic bytes: 2 reads of acc (count + emit) + 4 B per kept index
-// (+ 4 or 8 radix passes over acc for top-k).
+// (+ 3 or 6 radix passes over acc for top-k).
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -1815,38 +1815,52 @@ __global__ void set_delta_kernel(Ctrl* const* ctrls, int nctrl, const void* bits
 }
 
 // ---- K8: radix select of the pos-th smallest |v| (threshold.cpp:37-47) ------
-// The |v| bit patterns order like unsigned integers; 8-bit digits MSB first.
+// The |v| bit patterns order like unsigned integers; 11-bit digits MSB first
+// (3 passes over an fp32 vector, 6 over fp64; the last digit may be narrower).
+constexpr int kQBits = 11;
+constexpr int kQBins = 1 << kQBits;
+
 struct QState {
   unsigned long long prefix, mask;
   long long rank;
-  unsigned int hist[256];
+  unsigned int hist[kQBins];
 };
 
 template <typename T>
 __global__ void __launch_bounds__(256) quantile_hist_kernel(const T* v, int64_t m, QState* q,
-                                                            int shift) {
-  __shared__ unsigned int h[256];
-  h[threadIdx.x] = 0;
+                                                            int shift, unsigned int dmask) {
+  __shared__ unsigned int h[kQBins];
+  for (int i = threadIdx.x; i < kQBins; i += 256) h[i] = 0;
   __syncthreads();
   const unsigned long long prefix = q->prefix, mask = q->mask;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long b = Bits<T>::abs_bits(v[i]);
-    if ((b & mask) == prefix) atomicAdd(&h[(b >> shift) & 0xffu], 1u);
+    if ((b & mask) == prefix) atomicAdd(&h[(unsigned)(b >> shift) & dmask], 1u);
   }
   __syncthreads();
-  if (h[threadIdx.x]) atomicAdd(&q->hist[threadIdx.x], h[threadIdx.x]);
+  for (int i = threadIdx.x; i < kQBins; i += 256)
+    if (h[i]) atomicAdd(&q->hist[i], h[i]);
 }
 
-// One thread per digit: inclusive scan of the 256 bins in shared memory; the
-// digit whose [exclusive, inclusive) count range holds rank is the next digit.
-__global__ void __launch_bounds__(256) quantile_pick_kernel(QState* q, int shift) {
+// 256 threads, 8 consecutive bins each: block scan of the thread sums, then
+// the thread whose range holds rank walks its bins to the next digit. Every
+// thread clears the bins it has read.
+__global__ void __launch_bounds__(256) quantile_pick_kernel(QState* q, int shift,
+                                                            unsigned int dmask) {
+  constexpr int P = kQBins / 256;
   __shared__ long long inc[256];
   const int i = threadIdx.x;
   const long long r = q->rank;
-  const long long v = q->hist[i];
-  q->hist[i] = 0;  // each thread clears the bin it has read
-  inc[i] = v;
+  unsigned int v[P];
+  long long mine = 0;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    v[j] = q->hist[i * P + j];
+    q->hist[i * P + j] = 0;
+    mine += v[j];
+  }
+  inc[i] = mine;
   __syncthreads();
   for (int o = 1; o < 256; o <<= 1) {
     const long long add = i >= o ? inc[i - o] : 0;
@@ -1854,21 +1868,27 @@ __global__ void __launch_bounds__(256) quantile_pick_kernel(QState* q, int shift
     inc[i] += add;
     __syncthreads();
   }
-  const long long excl = inc[i] - v;
-  if (v > 0 && r >= excl && r < inc[i]) {
+  long long excl = inc[i] - mine;
+  if (mine > 0 && r >= excl && r < inc[i]) {
+    int d = 0;
+    for (; d < P - 1; ++d) {
+      if (r < excl + (long long)v[d]) break;
+      excl += v[d];
+    }
     q->rank = r - excl;
-    q->prefix |= (unsigned long long)i << shift;
-    q->mask |= 0xffULL << shift;
+    q->prefix |= (unsigned long long)(i * P + d) << shift;
+    q->mask |= (unsigned long long)dmask << shift;
   }
 }
 
 template <typename T>
-__global__ void quantile_init_kernel(QState* q, int64_t pos) {
-  if (threadIdx.x != 0) return;
-  q->prefix = 0;
-  q->mask = 0;
-  q->rank = pos;
-  for (int i = 0; i < 256; ++i) q->hist[i] = 0;
+__global__ void __launch_bounds__(256) quantile_init_kernel(QState* q, int64_t pos) {
+  if (threadIdx.x == 0) {
+    q->prefix = 0;
+    q->mask = 0;
+    q->rank = pos;
+  }
+  for (int i = threadIdx.x; i < kQBins; i += 256) q->hist[i] = 0;
 }
 
 template <typename T>
@@ -1887,13 +1907,15 @@ cudaError_t quantile_t(const T* v, int64_t m, int64_t pos, QState* q, T* out, cu
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  quantile_init_kernel<T><<<1, 32, 0, s>>>(q, pos);
+  quantile_init_kernel<T><<<1, 256, 0, s>>>(q, pos);
   int64_t blocks = (m + 255) / 256;
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
   if (blocks < 1) blocks = 1;
-  for (int shift = Bits<T>::W - 8; shift >= 0; shift -= 8) {
-    quantile_hist_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(v, m, q, shift);
-    quantile_pick_kernel<<<1, 256, 0, s>>>(q, shift);
+  for (int hi = Bits<T>::W; hi > 0; hi -= kQBits) {
+    const int shift = hi > kQBits ? hi - kQBits : 0;
+    const unsigned int dmask = (1u << (hi - shift)) - 1u;
+    quantile_hist_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(v, m, q, shift, dmask);
+    quantile_pick_kernel<<<1, 256, 0, s>>>(q, shift, dmask);
   }
   quantile_out_kernel<T><<<1, 32, 0, s>>>(q, out);
   return cudaGetLastError();
