@@ -227,7 +227,8 @@ int exd_initial_threshold_device(const void* mags_dev, int64_t m, int32_t dtype,
 /* Baseline sparsifiers, baselines.hpp:25-34 / baselines.cpp:26-46 (SURVEY
  * §8f row f4), over a device vector acc (dtype elements, n_g long). Indices
  * are ascending int32 written to idx_dev (device, capacity cap); enqueued on
- * cuda_stream, which the call synchronises.
+ * cuda_stream, which the call synchronises. acc_dev must be 16-byte aligned
+ * (EXD_EINVAL otherwise; cudaMalloc'd buffers are).
  * topk_select: exactly k indices, largest |acc| first, ties toward the lower
  * index; EXD_EINVAL "topk_select: k out of range" unless 1 <= k <= n_g. */
 int exd_topk_select_device(const void* acc_dev, int64_t n_g, int32_t dtype, int64_t k,

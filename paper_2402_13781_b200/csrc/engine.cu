@@ -1159,6 +1159,8 @@ int baseline_select(const void* acc, int64_t n_g, int32_t dtype, int topk, int64
     return EXD_OK;
   }
   if (!acc || (!idx && cap > 0)) return set_err(EXD_EINVAL, "null argument");
+  if (reinterpret_cast<uintptr_t>(acc) % 16 != 0)
+    return set_err(EXD_EINVAL, "acc must be 16-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // Grow-only scratch per device, plus a pinned read-back slot; the call is
   // synchronous, so one caller at a time holds them.

@@ -127,3 +127,19 @@ def test_device_baselines_edge_cases():
     with pytest.raises(S.InvalidArgument):
         S.topk_select(torch.zeros(4, dtype=torch.int32, device="cuda:0"), 1)
     assert S.topk_select(two, 1).cpu().tolist() == [1]
+    with pytest.raises(S.InvalidArgument, match="16-byte aligned"):
+        S.hard_threshold_select(torch.ones(9, device="cuda:0")[1:], 0.5)
+
+
+@pytest.mark.gpu
+def test_device_quantile_unaligned_input():
+    # K8 falls back to scalar loads for a vector that is not 16-byte aligned
+    import torch
+    from paper_2402_13781_b200 import sparsim as S
+    base = np.random.default_rng(9).laplace(size=100_003).astype(np.float32)
+    t = torch.tensor(base, device="cuda:0")[1:]
+    mags = np.abs(base[1:].astype(np.float64))
+    m = mags.shape[0]
+    pos = min(m - 1, int(np.floor((1 - 0.01) * m)))
+    want = np.partition(mags, pos)[pos]
+    assert S.initial_threshold_device(t.data_ptr(), m, 0.01, "f32") == want
