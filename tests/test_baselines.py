@@ -54,6 +54,23 @@ def test_numpy_restatement_matches_unmodified_reference_fresh_inputs():
         O.ref_topk_select(np.array([1.0, 2.0]), 3)
 
 
+def test_c_abi_argument_checks_without_gpu():
+    # the range checks run before any CUDA call (engine.cu: baseline_select)
+    import ctypes as C
+    from paper_2402_13781_b200 import _abi as A
+    from paper_2402_13781_b200._lib import lib
+    L = lib()
+    rc = L.exd_topk_select_device(None, 0, A.EXD_F32, 1, None, 1, None)
+    assert rc == A.EXD_EINVAL and L.exd_last_error() == b"topk_select: k out of range"
+    rc = L.exd_topk_select_device(None, 2, A.EXD_F32, 3, None, 3, None)
+    assert rc == A.EXD_EINVAL and L.exd_last_error() == b"topk_select: k out of range"
+    rc = L.exd_topk_select_device(None, 2, 7, 1, None, 1, None)
+    assert rc == A.EXD_EINVAL and L.exd_last_error() == b"dtype out of range"
+    cnt = C.c_int64(-1)
+    rc = L.exd_hard_threshold_select_device(None, 0, A.EXD_F64, 0.5, None, 0, C.byref(cnt), None)
+    assert rc == A.EXD_OK and cnt.value == 0
+
+
 # ---------------------------------------------------------------- GPU -------
 def _dev(acc, dtype):
     import torch
