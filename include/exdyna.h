@@ -227,8 +227,9 @@ int exd_initial_threshold_device(const void* mags_dev, int64_t m, int32_t dtype,
 /* Baseline sparsifiers, baselines.hpp:25-34 / baselines.cpp:26-46 (SURVEY
  * §8f row f4), over a device vector acc (dtype elements, n_g long). Indices
  * are ascending int32 written to idx_dev (device, capacity cap); enqueued on
- * cuda_stream, which the call synchronises. acc_dev must be 16-byte aligned
- * (EXD_EINVAL otherwise; cudaMalloc'd buffers are).
+ * cuda_stream, which the call synchronises, on the device that owns acc_dev.
+ * Any element alignment is accepted (16-byte aligned vectors take 128-bit
+ * loads, others a scalar path).
  * topk_select: exactly k indices, largest |acc| first, ties toward the lower
  * index; EXD_EINVAL "topk_select: k out of range" unless 1 <= k <= n_g. */
 int exd_topk_select_device(const void* acc_dev, int64_t n_g, int32_t dtype, int64_t k,
@@ -267,8 +268,11 @@ int32_t exd_engine_sync_mode(const exd_engine* h);
 void* exd_engine_stream(const exd_engine* h, int32_t w);
 
 /* Engine::step, engine.cpp:274-350. grads[w] is the device gradient of local
- * worker w (dtype elements, n_g long), produced on or before that worker's
- * stream. Blocks until the record is on the host. */
+ * worker w (dtype elements, n_g long, 16-byte aligned: the stream kernel reads
+ * it with 128-bit loads; EXD_EINVAL "gradient pointer must be 16-byte aligned"
+ * otherwise), produced on or before that worker's stream. Blocks until the
+ * record is on the host. After a peer-memory sync timeout (EXD_ENCCL) the
+ * engine refuses further steps. */
 int exd_engine_step(exd_engine* h, const void* const* grads_dev, exd_record* out);
 /* Enqueue one step without waiting for its record. */
 int exd_engine_step_async(exd_engine* h, const void* const* grads_dev);

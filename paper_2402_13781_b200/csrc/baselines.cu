@@ -41,6 +41,7 @@ struct Cut {
   int topk;                  // 1: strict = bits > cut, tie = bits == cut; 0: |a| >= delta
   double delta;
   const void* cut_bits;      // device: |value| bits of the k-th largest (top-k)
+  int vec;                   // acc is 16-byte aligned: 128-bit loads (else scalar)
 };
 
 // Layout of one tile: warp w owns the contiguous 32*PER elements (1024 f32 /
@@ -64,7 +65,7 @@ __device__ __forceinline__ void classify(const T* acc, int64_t n_g, int64_t wbas
   constexpr int V = Lay<T>::V, S = Lay<T>::S;
   const int lane = threadIdx.x & 31;
   T r[Lay<T>::PER];
-  if (wbase + 32 * Lay<T>::PER <= n_g) {
+  if (c.vec && wbase + 32 * Lay<T>::PER <= n_g) {
     const int4* p = reinterpret_cast<const int4*>(acc + wbase) + lane;
 #pragma unroll
     for (int i = 0; i < S; ++i) reinterpret_cast<int4*>(r)[i] = __ldg(p + 32 * i);
@@ -295,7 +296,7 @@ size_t baseline_scratch_bytes(int64_t n_g) {
 cudaError_t launch_baseline_select(const void* acc, int64_t n_g, int dtype, int topk, int64_t k,
                                    double delta, int32_t* out, int64_t cap, int64_t* totals_dev,
                                    void* scratch, cudaStream_t s) {
-  Cut c{topk, delta, nullptr};
+  Cut c{topk, delta, nullptr, (reinterpret_cast<uintptr_t>(acc) & 15u) == 0 ? 1 : 0};
   char* base = static_cast<char*>(scratch);
   char* qscratch = base + (baseline_scratch_bytes(n_g) - quantile_scratch_bytes() - 64);
   char* cut_bits = qscratch + quantile_scratch_bytes();

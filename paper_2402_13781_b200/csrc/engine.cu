@@ -260,6 +260,7 @@ struct exd_engine {
   std::vector<cudaEvent_t> free_ev;
   exd_kernel_stats stats{};
   bool has_record = false;
+  bool broken = false;                // a peer timed out: further steps are refused
 };
 
 namespace {
@@ -766,8 +767,13 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   const exd_config& c = h->cfg;
   const int n = h->n;
   const int nl = (int)h->w.size();
-  for (int i = 0; i < nl; ++i)
+  if (h->broken) return set_err(EXD_ENCCL, "engine unusable after a peer-memory sync timeout");
+  for (int i = 0; i < nl; ++i) {
     if (!grads || !grads[i]) return set_err(EXD_EINVAL, "null gradient pointer");
+    // the stream kernel reads g with 16-byte vector loads
+    if (reinterpret_cast<uintptr_t>(grads[i]) % 16 != 0)
+      return set_err(EXD_EINVAL, "gradient pointer must be 16-byte aligned");
+  }
   CU(cudaSetDevice(h->device));
 
   // verify_conservation (engine.cpp:142): acc snapshot of every worker
@@ -791,7 +797,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
     if (!h->dist || h->w[0].rank == 0)
     {
       CU(launch_quantile(h->w[0].e, m, pos, h->opt.dtype, h->qscratch, h->qbits, h->stream));
-      h->stats.kernel_launches += 2 + 2 * (int64_t)(8 * h->esz / 8);
+      h->stats.kernel_launches += quantile_launches(h->opt.dtype);
     }
     if (h->dist && n > 1)
       NC(nccl().Broadcast(h->qbits, h->qbits, h->esz, ncclUint8, 0, h->comm, h->stream));
@@ -1022,8 +1028,11 @@ int sync_engine(exd_engine* h, exd_record* out) {
   h->pending.clear();
   if (h->p2p) {
     CU(cudaMemcpy(h->p2p_err, h->p2p_err_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost));
-    if (*h->p2p_err)
+    if (*h->p2p_err) {
+      // the in-kernel counters and epochs no longer line up across ranks
+      h->broken = true;
       return set_err(EXD_ENCCL, "peer-memory sync: a peer did not arrive within 20 s");
+    }
   }
   if (*h->verify_flag) {
     const uint32_t f = *h->verify_flag;
@@ -1159,8 +1168,21 @@ int baseline_select(const void* acc, int64_t n_g, int32_t dtype, int topk, int64
     return EXD_OK;
   }
   if (!acc || (!idx && cap > 0)) return set_err(EXD_EINVAL, "null argument");
-  if (reinterpret_cast<uintptr_t>(acc) % 16 != 0)
-    return set_err(EXD_EINVAL, "acc must be 16-byte aligned");
+  // run on the device that owns acc (the caller's current device may differ)
+  int prev = 0, dev = 0;
+  CU(cudaGetDevice(&prev));
+  dev = prev;
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, acc) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+      dev = pa.device;
+    cudaGetLastError();
+  }
+  if (dev != prev) CU(cudaSetDevice(dev));
+  struct Restore {
+    int d, p;
+    ~Restore() { if (d != p) cudaSetDevice(p); }
+  } restore{dev, prev};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // Grow-only scratch per device, plus a pinned read-back slot; the call is
   // synchronous, so one caller at a time holds them.
@@ -1171,8 +1193,6 @@ int baseline_select(const void* acc, int64_t n_g, int32_t dtype, int topk, int64
   };
   static std::mutex mu;
   static Scratch cache[64];
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return set_err(EXD_EINVAL, "device ordinal out of range");
   std::lock_guard<std::mutex> lock(mu);
   Scratch& sc = cache[dev];

@@ -219,6 +219,7 @@ cudaError_t launch_set_delta(Ctrl* const* ctrls, int nctrl, const void* src_bits
 cudaError_t launch_quantile(const void* v, int64_t m, int64_t pos, int dtype, void* scratch,
                             void* out_bits, cudaStream_t s);
 size_t quantile_scratch_bytes();
+int quantile_launches(int dtype);  // kernels one launch_quantile enqueues
 cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void* x0,
                                       const void* xw, int64_t n_g, int dtype, int32_t w,
                                       uint32_t* flag, cudaStream_t s);

@@ -1063,12 +1063,21 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
       esh.capped[r] = __ldcg(&a.inbox[r].capped);
     }
     __syncthreads();
+    // the counts are read: join the arrive counter, so block 0 publishes
+    // "contributions ready" (which lets the peers overwrite these inbox words
+    // in step t+1) only after this block is done with them
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&a.gate[2], 1ull);
+    }
     epi_run_store(esh, a.ctrl, rc, a.rec);
     PROBE(24);
     return;
   }
   if (tid == 0) {
-    const int64_t tm = mod_floor(a.ctrl->t, n);
+    // the step from the launch argument, not a.ctrl->t: block G's epilogue
+    // rewrites the control block (t + 1) concurrently
+    const int64_t tm = mod_floor((int64_t)a.epoch - 1, n);
     int64_t off = 0;
     for (int p = 0; p < n; ++p) {
       const int r = (int)mod_floor(p - tm, n);
@@ -1136,8 +1145,18 @@ __global__ void __launch_bounds__(256) p2p_sync_kernel(P2PArgs a, RunConst rc) {
   }
   if (blockIdx.x == 0) {
     if (tid == 0) {
-      const unsigned long long want = a.epoch * (unsigned long long)G;
-      while (*(volatile unsigned long long*)&a.gate[2] < want) __nanosleep(32);
+      // G work blocks + the epilogue block arrive once per step
+      const unsigned long long want = a.epoch * (unsigned long long)(G + 1);
+      const unsigned long long t0 = gtime_ns();
+      unsigned spins = 0;
+      while (*(volatile unsigned long long*)&a.gate[2] < want) {
+        if ((++spins & 255u) == 0 &&
+            (gtime_ns() - t0 > 20000000000ull || *(volatile unsigned int*)a.err)) {
+          atomicExch(a.err, 1u);  // the engine is unusable after this (sync reports it)
+          break;
+        }
+        __nanosleep(32);
+      }
       __threadfence();
     }
     __syncthreads();
@@ -2311,6 +2330,11 @@ cudaError_t launch_set_delta(Ctrl* const* ctrls, int nctrl, const void* bits, in
 }
 
 size_t quantile_scratch_bytes() { return sizeof(QState); }
+
+int quantile_launches(int dtype) {
+  const int w = dtype == EXD_F64 ? 64 : 32;
+  return 2 + 2 * ((w + kQBits - 1) / kQBits);  // init, (hist + pick) per digit, out
+}
 
 cudaError_t launch_quantile(const void* v, int64_t m, int64_t pos, int dtype, void* scratch,
                             void* out_bits, cudaStream_t s) {

@@ -208,8 +208,10 @@ def topk_select(acc, k: int):
     import torch
     ptr, n_g, code = _acc_args(acc)
     out = torch.empty(max(k, 0), dtype=torch.int32, device=acc.device)
-    check(lib().exd_topk_select_device(C.c_void_p(ptr), n_g, code, k, C.c_void_p(out.data_ptr()),
-                                       out.numel(), _stream_of(acc)))
+    with torch.cuda.device(acc.device):
+        check(lib().exd_topk_select_device(C.c_void_p(ptr), n_g, code, k,
+                                           C.c_void_p(out.data_ptr()), out.numel(),
+                                           _stream_of(acc)))
     return out
 
 
@@ -220,9 +222,11 @@ def hard_threshold_select(acc, fixed_delta: float):
     ptr, n_g, code = _acc_args(acc)
     out = torch.empty(n_g, dtype=torch.int32, device=acc.device)
     cnt = C.c_int64()
-    check(lib().exd_hard_threshold_select_device(C.c_void_p(ptr), n_g, code, float(fixed_delta),
-                                                 C.c_void_p(out.data_ptr()), out.numel(),
-                                                 C.byref(cnt), _stream_of(acc)))
+    with torch.cuda.device(acc.device):
+        check(lib().exd_hard_threshold_select_device(C.c_void_p(ptr), n_g, code,
+                                                     float(fixed_delta),
+                                                     C.c_void_p(out.data_ptr()), out.numel(),
+                                                     C.byref(cnt), _stream_of(acc)))
     return out[:cnt.value]
 
 
@@ -406,7 +410,22 @@ class Engine:
             raise InvalidArgument("one gradient per local worker")
         ps = []
         for g in grads:
-            ps.append(g if isinstance(g, int) else g.data_ptr())
+            if isinstance(g, int):  # a raw device pointer: the C ABI checks null / alignment
+                ps.append(g)
+                continue
+            import torch
+            want = torch.float64 if self.np_dtype == np.float64 else torch.float32
+            if not (isinstance(g, torch.Tensor) and g.is_cuda):
+                raise InvalidArgument("gradient must be a CUDA tensor or a device pointer")
+            if g.dtype != want:
+                raise InvalidArgument(f"gradient dtype {g.dtype} != engine dtype {want}")
+            if g.numel() != self.cfg.n_g or not g.is_contiguous():
+                raise InvalidArgument("engine: workload size != n_g")
+            if g.device.index != self.device:
+                raise InvalidArgument(f"gradient on {g.device}, engine on cuda:{self.device}")
+            if g.data_ptr() % 16:
+                raise InvalidArgument("gradient pointer must be 16-byte aligned")
+            ps.append(g.data_ptr())
         return (C.c_void_p * len(ps))(*ps)
 
     def step(self, grads) -> IterationRecord:

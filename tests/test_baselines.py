@@ -144,8 +144,35 @@ def test_device_baselines_edge_cases():
     with pytest.raises(S.InvalidArgument):
         S.topk_select(torch.zeros(4, dtype=torch.int32, device="cuda:0"), 1)
     assert S.topk_select(two, 1).cpu().tolist() == [1]
-    with pytest.raises(S.InvalidArgument, match="16-byte aligned"):
-        S.hard_threshold_select(torch.ones(9, device="cuda:0")[1:], 0.5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_device_baselines_unaligned_view(dtype):
+    # a tensor view that is not 16-byte aligned takes the scalar-load path
+    import torch
+    from paper_2402_13781_b200 import sparsim as S
+    base = np.random.default_rng(5).laplace(size=300_001).astype(dtype)
+    view = torch.tensor(base, device="cuda:0")[1:]
+    assert view.data_ptr() % 16 != 0
+    got = S.hard_threshold_select(view, 1.5).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.hard_threshold_select_np(base[1:], 1.5))
+    got = S.topk_select(view, 3001).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.topk_select_np(base[1:], 3001))
+
+
+@pytest.mark.gpu
+def test_device_baselines_follow_the_tensor_device():
+    # acc on cuda:1 while the current device is cuda:0
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_2402_13781_b200 import sparsim as S
+    acc = np.random.default_rng(6).laplace(size=100_000).astype(np.float32)
+    torch.cuda.set_device(0)
+    t = torch.tensor(acc, device="cuda:1")
+    got = S.hard_threshold_select(t, 2.0).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.hard_threshold_select_np(acc, 2.0))
 
 
 @pytest.mark.gpu

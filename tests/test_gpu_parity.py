@@ -289,6 +289,22 @@ def test_kernel_stats_and_unsupported_options():
     st = eng.kernel_stats()
     # t=0 without delta0: accumulate + select-only launches, then one fused launch per step
     assert st["select_launches"] == 4 and st["select_ms"] > 0 and st["steps"] == 3
+    # t = 0: accumulate, K8 (init + 3 x (hist + pick) + out for fp32), set_delta,
+    # select-only + finish; then stream + finish per step
+    assert st["kernel_launches"] == 1 + 8 + 1 + 2 + 2 * 2
+    # gradients must be 16-byte aligned, the right dtype and n_g long
+    flat = torch.zeros(100_004, device="cuda")
+    with pytest.raises(S.InvalidArgument, match="16-byte aligned"):
+        eng.step([flat[1:100_001]])
+    with pytest.raises(S.InvalidArgument, match="workload size"):
+        eng.step([flat])
+    with pytest.raises(S.InvalidArgument, match="dtype"):
+        eng.step([flat[:100_000].double()])
+    from paper_2402_13781_b200._lib import lib
+    import ctypes as C
+    rc = lib().exd_engine_step_async(eng.h, (C.c_void_p * 1)(flat.data_ptr() + 4))
+    assert rc == S.A.EXD_EINVAL
+    eng.step([flat[:100_000]])  # the engine is still usable
 
 
 CAP_CONFIGS = [
