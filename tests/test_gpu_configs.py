@@ -9,8 +9,10 @@
            acceptance_main.cpp:234-248).
   * R18    (n_g = 11.2M, d = 0.01, n = 8): bit-exact steps + structural
            properties (ascending union, exclusive ownership, conservation).
-  * sweep  (n_g up to 1B): size-independent properties of one step, checked
-           on the device.
+  * sweep  (configs[4], n_g 10M / 100M / 1B): multi-step trajectories
+           bit-exact vs the fp32 oracle (records, selections, per-block
+           counts, delta, topology, and x / e at the end), plus size-
+           independent properties of one step checked on the device.
 """
 import numpy as np
 import pytest
@@ -122,6 +124,49 @@ def test_r18_n8_full_size_bit_exact_and_structural():
     for w in range(8):
         assert not np.any(p.eng.e(w)[u])
     assert st.t == 6
+
+
+def _host_bytes_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+SWEEP_CELLS = [
+    # n_g, d, n, steps
+    (10_000_000, 0.001, 1, 30),
+    (10_000_000, 0.1, 2, 30),
+    (100_000_000, 0.01, 1, 30),
+    (100_000_000, 0.001, 2, 20),
+    (100_000_000, 0.1, 1, 12),
+    (1_000_000_000, 0.01, 1, 3),
+]
+
+
+@pytest.mark.parametrize("n_g,d,n,steps", SWEEP_CELLS,
+                         ids=lambda v: str(v))
+def test_sweep_multi_step_bit_exact_vs_oracle(n_g, d, n, steps):
+    """configs[4] cells: the whole trajectory (t = 0 quantile, adjust, delta
+    scaling) equals the fp32 restatement of engine.cpp:274-350 step by step."""
+    import torch
+    free, _ = torch.cuda.mem_get_info(0)
+    if free < 40 * n * n_g:
+        pytest.skip("not enough device memory")
+    if _host_bytes_available() < 40 * n * n_g:
+        pytest.skip("not enough host memory for the oracle")
+    kw = _pinned(n=n, n_g=n_g, d=d, seed=7)
+    p = Pair(kw, "f32", verify_replication=False)
+    for t in range(steps):
+        rec, orec = p.step(t)
+        check_record(rec, orec, ctx=f"t={t}")
+        if t % 10 == 9 or t == steps - 1:
+            p.compare_selection(ctx=f"t={t}")
+    p.compare_state(ctx="end", vectors=True)
+    assert rec.t == steps - 1
 
 
 @pytest.mark.parametrize("n_g,d", [(1_000_000, 0.1), (100_000_000, 0.001), (1_000_000_000, 0.01)])
