@@ -380,13 +380,23 @@ def ncu_traffic(args, timeout=240):
     if not rows:
         return {"source": f"unavailable: ncu rc={r.returncode}: {r.stderr[-300:]}"}
     launches = {}
-    for row in csv.DictReader(io.StringIO("\n".join(rows))):
+    try:
+        return ncu_parse(csv.DictReader(io.StringIO("\n".join(rows))), launches)
+    except Exception as e:
+        return {"source": f"unavailable: ncu output not parsed: {e}"}
+
+
+def ncu_parse(reader, launches):
+    for row in reader:
         key = (row["ID"], row["Kernel Name"])
         d = launches.setdefault(key, {"name": row["Kernel Name"]})
         unit = row.get("Metric Unit", "")
         val = float(row["Metric Value"].replace(",", ""))
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-                 "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
+        scale = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6,
+                 "Gbyte": 1e9, "GB": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6,
+                 "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}.get(unit)
+        if scale is None:
+            raise ValueError(f"ncu unit {unit!r} of {row['Metric Name']}")
         d[row["Metric Name"]] = val * scale
     order = sorted(launches, key=lambda k: int(k[0]))
 
@@ -430,7 +440,7 @@ def device_grad_fn(S, torch, wl, local, stream_ptr):
     return fn
 
 
-def variant_run(S, torch, base_wl, local, dtype, beta, steps=60):
+def variant_run(S, torch, base_wl, local, dtype, beta, steps=400):
     """A fresh engine from t = 0 on the fp32-rounded device stream, timed per
     step like the main line (L2 flushed, CUDA events on the engine stream)."""
     wl = Workload(1, n_g=base_wl.n_g, d=base_wl.d, dtype=dtype, beta=beta)
@@ -469,15 +479,19 @@ def variants(S, torch, wl, local, budget_s, stream_ptr):
     out = []
     for dtype, beta in (("f64", 1.25), ("f32", 1.05)):
         vwl, ms, recs = variant_run(S, torch, wl, local, dtype, beta)
+        steady = recs[len(recs) // 2:]  # the controller has settled (delta moves 2% a step)
         item = {"dtype": dtype, "beta": beta, "steps": len(ms),
                 "step_ms_median_t_ge_5": statistics.median(ms[5:]),
                 "step_ms_mean_t_ge_5": statistics.mean(ms[5:]),
-                "density_mean_t_ge_5": statistics.mean(r.density for r in recs[5:]),
-                "density_over_d": statistics.mean(r.density for r in recs[5:]) / wl.d}
+                "density_mean_steady": statistics.mean(r.density for r in steady),
+                "density_over_d_steady": statistics.mean(r.density for r in steady) / wl.d,
+                "steady_window": [steady[0].t, steady[-1].t]}
         try:
+            # the reference on the same inputs for the first 60 steps: its
+            # timing, and its density / records next to the GPU's
             rms, rtimes, rrecs = cpu_run("reference", vwl, device_grad_fn(S, torch, vwl, local,
                                                                           stream_ptr),
-                                         steps=len(ms) - 5, warmup=5, budget_s=budget_s)
+                                         steps=55, warmup=5, budget_s=budget_s)
             m = min(len(rrecs), len(recs))
             item["reference"] = {
                 "median_ms": rms, "steps_timed": len(rtimes), "steps": m,

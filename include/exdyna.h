@@ -278,6 +278,11 @@ int exd_engine_step(exd_engine* h, const void* const* grads_dev, exd_record* out
 int exd_engine_step_async(exd_engine* h, const void* const* grads_dev);
 /* Wait for all enqueued steps; *out (may be NULL) gets the last record. */
 int exd_engine_sync(exd_engine* h, exd_record* out);
+/* Records of steps [first, first + count) after waiting for all enqueued steps
+ * (Engine::run's record vector, engine.cpp:352-358). The device keeps the
+ * last EXD_RECORD_RING steps; older ones give EXD_EINVAL. */
+#define EXD_RECORD_RING 256
+int exd_engine_records(exd_engine* h, int64_t first, int64_t count, exd_record* out);
 /* Host-buffer step (GradientSource::gradient fills host memory,
  * workloads.hpp:77-87): copies grads_host[w] to the device on worker w's
  * stream, steps, and returns the record. */

@@ -87,6 +87,7 @@ def lib():
     _sig(L, "exd_engine_step", C.c_int, [P, C.POINTER(P), C.POINTER(A.exd_record)])
     _sig(L, "exd_engine_step_async", C.c_int, [P, C.POINTER(P)])
     _sig(L, "exd_engine_sync", C.c_int, [P, C.POINTER(A.exd_record)])
+    _sig(L, "exd_engine_records", C.c_int, [P, C.c_int64, C.c_int64, C.POINTER(A.exd_record)])
     _sig(L, "exd_engine_step_host", C.c_int, [P, C.POINTER(P), C.POINTER(A.exd_record)])
     _sig(L, "exd_engine_get_state", C.c_int, [P, C.c_int32, C.POINTER(A.exd_worker_state)])
     _sig(L, "exd_engine_copy_out", C.c_int, [P, C.c_int32, C.c_int32, P, C.c_int64, PI64])
@@ -128,6 +129,7 @@ EXPORTED = [
     "exd_engine_local_workers", "exd_engine_first_rank", "exd_engine_iteration",
     "exd_engine_sync_mode",
     "exd_engine_stream", "exd_engine_step", "exd_engine_step_async", "exd_engine_sync",
+    "exd_engine_records",
     "exd_engine_step_host", "exd_engine_get_state", "exd_engine_copy_out", "exd_engine_copy_in",
     "exd_engine_device_vector",
     "exd_engine_kernel_stats", "exd_engine_reset_kernel_stats", "exd_engine_set_profile",

@@ -15,11 +15,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -44,6 +47,15 @@ int set_err(int code, const std::string& msg) {
     if (_e != cudaSuccess)                                                         \
       return set_err(EXD_ECUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e)); \
   } while (0)
+
+double nccl_timeout_s() {
+  static double v = [] {
+    const char* e = std::getenv("EXD_NCCL_TIMEOUT_S");
+    const double d = e ? std::atof(e) : 0.0;
+    return d > 0.0 ? d : 60.0;
+  }();
+  return v;
+}
 
 // ---- validate(), config.cpp:28-51 -----------------------------------------
 int validate_cfg(const exd_config* in, exd_config* out) {
@@ -104,6 +116,8 @@ struct Nccl {
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclBroadcast) Broadcast = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+  decltype(&ncclCommAbort) CommAbort = nullptr;
   bool ok = false;
   std::string why;
 };
@@ -125,9 +139,11 @@ Nccl& nccl() {
     SYM(AllReduce);
     SYM(Broadcast);
     SYM(GetErrorString);
+    SYM(CommGetAsyncError);
+    SYM(CommAbort);
 #undef SYM
     n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllGather && n.AllReduce &&
-           n.Broadcast && n.GetErrorString;
+           n.Broadcast && n.GetErrorString && n.CommGetAsyncError && n.CommAbort;
     if (!n.ok) n.why = "libnccl.so.2 lacks a required symbol";
   });
   return n;
@@ -163,7 +179,7 @@ void blk_magic(int64_t d, unsigned long long* magic, int32_t* shift) {
 }
 
 // per-step records stay on the device; the host copies the latest at sync
-constexpr int64_t kRecRing = 256;
+constexpr int64_t kRecRing = EXD_RECORD_RING;
 
 }  // namespace
 
@@ -264,6 +280,42 @@ struct exd_engine {
 };
 
 namespace {
+
+// Host wait for the engine's stream. With a communicator, poll instead of
+// blocking: ncclCommGetAsyncError reports a failed collective, and a
+// collective stuck on a dead peer gives up after EXD_NCCL_TIMEOUT_S (60 s).
+// Either way the communicator is aborted, the engine refuses further steps
+// and the call returns EXD_ENCCL (the reference's analogue is an EngineError
+// out of step(), engine.cpp:251-272).
+int wait_stream(exd_engine* h) {
+  if (!h->comm) {
+    CU(cudaStreamSynchronize(h->stream));
+    return EXD_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(h->stream);
+    if (e == cudaSuccess) return EXD_OK;
+    if (e != cudaErrorNotReady)
+      return set_err(EXD_ECUDA, std::string("engine stream: ") + cudaGetErrorString(e));
+    ncclResult_t ar = ncclSuccess;
+    nccl().CommGetAsyncError(h->comm, &ar);
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || el > nccl_timeout_s()) {
+      const std::string why =
+          ar != ncclSuccess && ar != ncclInProgress
+              ? std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ar)
+              : "NCCL collective did not complete within " + std::to_string((int)nccl_timeout_s()) +
+                    " s (a peer is gone?)";
+      nccl().CommAbort(h->comm);
+      h->comm = nullptr;
+      h->broken = true;
+      return set_err(EXD_ENCCL, why);
+    }
+    if (spin > 1000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
 
 int alloc_zero(void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
@@ -424,6 +476,10 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
 void teardown(exd_engine* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->broken && h->comm) {  // a peer is gone: no teardown barrier with it
+    nccl().CommAbort(h->comm);
+    h->comm = nullptr;
+  }
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->p2p && h->comm) {
     // barrier: no peer may still be reading our region when it is freed
@@ -722,6 +778,8 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.push_idx = (h->p2p && !h->xchg && h->cap == 0) ? h->d_push : nullptr;
   a.npush = (h->p2p && !h->xchg && h->cap == 0) ? h->n - 1 : 0;
   a.k1_npush = h->xchg ? h->n : 0;  // every peer, then this rank's own inbox
+  // pairs of ~2k/n selections (16 B fp64, 8 B fp32) against a 32 MB share of L2
+  a.stage_keep = 2 * (double)h->cfg.k / h->n * (h->esz == 8 ? 16 : 8) < 32e6 ? 1 : 0;
   const int par = (int)(h->t & 1);  // this step's parity slots
   for (int q = 0; q < a.k1_npush; ++q) {
     a.push_stage[q] = h->push_stage[par][q];
@@ -767,7 +825,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
   const exd_config& c = h->cfg;
   const int n = h->n;
   const int nl = (int)h->w.size();
-  if (h->broken) return set_err(EXD_ENCCL, "engine unusable after a peer-memory sync timeout");
+  if (h->broken) return set_err(EXD_ENCCL, "engine unusable after a failed collective (peer timeout or NCCL error)");
   for (int i = 0; i < nl; ++i) {
     if (!grads || !grads[i]) return set_err(EXD_EINVAL, "null gradient pointer");
     // the stream kernel reads g with 16-byte vector loads
@@ -868,7 +926,7 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));
       CU(cudaMemcpyAsync(h->counts_host, h->counts_all, sizeof(CountRec) * n,
                          cudaMemcpyDeviceToHost, h->stream));
-      CU(cudaStreamSynchronize(h->stream));
+      if (int rc = wait_stream(h)) return rc;
       int64_t m_t = 0, kp = 0;
       for (int r = 0; r < n; ++r) {
         m_t = h->counts_host[r].k > m_t ? h->counts_host[r].k : m_t;
@@ -1010,7 +1068,7 @@ void finalize_record(const RawRecord& r, const exd_config& cfg, exd_record* rec)
 
 int sync_engine(exd_engine* h, exd_record* out) {
   CU(cudaSetDevice(h->device));
-  CU(cudaStreamSynchronize(h->stream));
+  if (int rc = wait_stream(h)) return rc;
   for (auto& p : h->pending) {
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -1332,6 +1390,26 @@ int exd_engine_step_async(exd_engine* h, const void* const* grads_dev) {
 }
 
 int exd_engine_sync(exd_engine* h, exd_record* out) { return sync_engine(h, out); }
+
+int exd_engine_records(exd_engine* h, int64_t first, int64_t count, exd_record* out) {
+  if (int rc = sync_engine(h, nullptr)) return rc;
+  if (count == 0) return EXD_OK;
+  if (!out || count < 0 || first < 0 || first + count > h->t)
+    return set_err(EXD_EINVAL, "record range out of range");
+  if (h->t - first > kRecRing) return set_err(EXD_EINVAL, "records no longer on the device");
+  std::vector<RawRecord> raw((size_t)count);
+  const Worker& wk = h->w[0];
+  int64_t done = 0;
+  while (done < count) {  // the ring may wrap
+    const int64_t slot = (first + done) % kRecRing;
+    const int64_t run = std::min<int64_t>(count - done, kRecRing - slot);
+    CU(cudaMemcpy(raw.data() + done, wk.rec_dev + slot, sizeof(RawRecord) * (size_t)run,
+                  cudaMemcpyDeviceToHost));
+    done += run;
+  }
+  for (int64_t i = 0; i < count; ++i) finalize_record(raw[(size_t)i], h->cfg, out + i);
+  return EXD_OK;
+}
 
 int exd_engine_step(exd_engine* h, const void* const* grads_dev, exd_record* out) {
   if (int rc = enqueue_step(h, grads_dev)) return rc;

@@ -109,6 +109,9 @@ struct SelectArgs {
   unsigned long long* push_chunk[EXD_MAX_WORKERS];  // [k1_npush] my per-chunk count slot
   unsigned long long* push_tile[EXD_MAX_WORKERS];   // [k1_npush] my per-tile count slot
   int32_t k1_npush;             // 0: no pushes
+  int32_t stage_keep;           // staged pairs small enough to keep in L2 (evict_last);
+                                // else streamed (evict_first) so they do not crowd the
+                                // 126 MB L2 at large k
 };
 
 constexpr int kMaxCtas = 2048;

@@ -179,15 +179,41 @@ __device__ EXD_EPI_INLINE void make_plan(Plan* p, const exd_topology* base, cons
   p->end = end;
 }
 
-__device__ EXD_EPI_INLINE void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc) {
+// The three outcomes of scale_threshold (threshold.cpp:23-35) for the current
+// delta, computed before the step's counts are known: delta * sf with the same
+// operations as scale_threshold_r, so picking one by the band of k'/k later is
+// bit-identical to calling it.
+__device__ __forceinline__ void delta_candidates(double delta, const RunConst& rc, double* dc,
+                                                 float* tc) {
+  dc[0] = dmul(delta, dadd(1.0, rc.gamma));
+  dc[1] = dmul(delta, dadd(1.0, dmul(0.25, rc.gamma)));
+  dc[2] = dmul(delta, dadd(1.0, -rc.gamma));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tc[i] = thr_of(dc[i]);
+}
+
+__device__ __forceinline__ int delta_band(int64_t k_prime, const RunConst& rc) {
+  const double exam = ddiv((double)k_prime, (double)rc.k);
+  return exam > rc.beta ? 0 : exam > rc.inv_beta ? 1 : 2;
+}
+
+// dc/tc: precomputed candidates (delta_candidates) or nullptr
+__device__ EXD_EPI_INLINE void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc,
+                                             const double* dc, const float* tc) {
   const int n = rc.n;
   int64_t kp = 0;
   for (int r = 0; r < n; ++r) {
     kp += k_rank[r];
     c->k_t[r] = k_rank[r];
   }
-  c->delta = scale_threshold_r(rc.k, kp, c->delta, rc.beta, rc.inv_beta, rc.gamma);
-  c->thr_f = thr_of(c->delta);
+  if (dc) {
+    const int b = delta_band(kp, rc);
+    c->delta = dc[b];
+    c->thr_f = tc[b];
+  } else {
+    c->delta = scale_threshold_r(rc.k, kp, c->delta, rc.beta, rc.inv_beta, rc.gamma);
+    c->thr_f = thr_of(c->delta);
+  }
   const Plan* cur = &c->plan[c->t & 1];
   copy_topo(&c->topo, &cur->topo, n);
   copy_topo(&c->last.topo, &cur->topo, n);
@@ -207,10 +233,36 @@ struct EpiShared {
   double norm2[EXD_MAX_WORKERS];
   int64_t capped[EXD_MAX_WORKERS];
   int64_t scratch[EXD_MAX_WORKERS];  // make_plan's partition-order counts
+  // epi_prepare (before the counts are in): the three delta outcomes, and step
+  // t+1's plan when it does not depend on the counts (n == 1, static partitions)
+  double dcand[3];
+  float tcand[3];
+  int32_t prepared;
+  int32_t plan_ready;
 };
+
+// Count-independent half of the epilogue, run while the counts are still being
+// produced (sh.c loaded and synced by the caller). Whole CTA.
+__device__ __forceinline__ void epi_prepare(EpiShared& sh, const RunConst& rc) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    delta_candidates(sh.c.delta, rc, sh.dcand, sh.tcand);
+    sh.prepared = 1;
+  } else if (tid == 32) {
+    const bool free_plan = rc.n == 1 || rc.static_partitions;
+    if (free_plan) {
+      const int64_t t = sh.c.t;
+      const int tm_next = sh.c.tmod + 1 == rc.n ? 0 : sh.c.tmod + 1;
+      make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc,
+                sh.scratch);
+    }
+    sh.plan_ready = free_plan ? 1 : 0;
+  }
+}
 
 __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
   static_assert(sizeof(Ctrl) % 8 == 0, "word copies");
+  if (threadIdx.x == 0) sh.prepared = sh.plan_ready = 0;
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
   const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(cg);
   constexpr int W = (int)(sizeof(Ctrl) / 8);
@@ -228,11 +280,14 @@ __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const Run
   const double delta_used = sh.c.delta;
   __syncthreads();  // everyone read t / tmod / delta before warp 0 changes them
   if (tid == 0) {
-    advance_delta(&sh.c, sh.k_rank, rc);
+    advance_delta(&sh.c, sh.k_rank, rc, sh.prepared ? sh.dcand : nullptr,
+                  sh.prepared ? sh.tcand : nullptr);
     sh.c.done = 0;
     PROBE_ANY(26);
   } else if (tid == 32) {
-    make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc, sh.scratch);
+    if (!sh.plan_ready)
+      make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc,
+                sh.scratch);
     PROBE_ANY(27);
   } else if (tid == 64 && rec_out) {
     const Plan& cur = sh.c.plan[t & 1];
@@ -292,7 +347,7 @@ template <> struct Pair<float> {
   __device__ static P make(uint32_t j, float v) { return make_uint2(j, __float_as_uint(v)); }
   __device__ static uint32_t idx(const P& p) { return p.x; }
   __device__ static float val(const P& p) { return __uint_as_float(p.y); }
-  __device__ static void store_keep(P* q, const P& p, uint64_t pol) {  // L2 evict_last
+  __device__ static void store_keep(P* q, const P& p, uint64_t pol) {  // L2 policy `pol`
     asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(q), "r"(p.x), "r"(p.y),
                  "l"(pol) : "memory");
   }
@@ -485,7 +540,10 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
     const bool split = b_lo != b_hi;
     uint64_t keep;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    if (a.stage_keep)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    else
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(keep));
     typename Pair<T>::P* sp = static_cast<typename Pair<T>::P*>(a.stage);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -634,7 +692,11 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     // ---- epilogue CTA: prefetch the control block (n == 1), then the totals
     // in a fixed order, then the control epilogue
     __shared__ EpiShared esh;
-    if (FUSED) epi_load(esh, ctrl);  // the stream kernel never writes the control block
+    if (FUSED) {
+      epi_load(esh, ctrl);  // the stream kernel never writes the control block
+      __syncthreads();
+      epi_prepare(esh, rc);
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // next step's block counters (nobody reads that parity during this step)
     for (int i = tid; i < rc.n_b; i += kThreads) a.blk_next[i] = 0;
@@ -1325,6 +1387,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int64_t st = plan.st, end = plan.end;
     const int ft = (int)(st / TILE), lt = (int)((end - 1) / TILE);
     epi_load(esh, ctrl);  // the stream kernel never writes the control block
+    __syncthreads();
+    epi_prepare(esh, rc);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) PROBE(0);
     for (int i = tid; i < rc.n_b; i += kThreads) sa.blk_next[i] = 0;

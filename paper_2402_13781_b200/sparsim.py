@@ -451,14 +451,28 @@ class Engine:
         return IterationRecord.from_c(rec)
 
     def run(self, iterations, source, device_bufs):
-        """Engine::run (engine.cpp:352-357) over a device GradientSource."""
+        """Engine::run (engine.cpp:352-357) over a device GradientSource: the
+        generator and the steps are stream-ordered on the engine's stream, so
+        steps are only enqueued here; the records are fetched in batches."""
         out = []
-        for _ in range(iterations):
+        first = self.iteration()
+        for i in range(iterations):
             t = self.iteration()
             for w, buf in enumerate(device_bufs):
                 source.gradient(t, self.first_rank + w, buf, self.opt.dtype, self.stream(w))
-            out.append(self.step(device_bufs))
+            self.step_async(device_bufs)
+            if (i + 1) % 128 == 0 or i + 1 == iterations:
+                out.extend(self.records(first + len(out), i + 1 - len(out)))
         return out
+
+    def records(self, first, count):
+        """IterationRecords of steps [first, first + count) (the device keeps
+        the last EXD_RECORD_RING)."""
+        if count <= 0:
+            return []
+        buf = (A.exd_record * count)()
+        check(self.L.exd_engine_records(self.h, first, count, buf))
+        return [IterationRecord.from_c(r) for r in buf]
 
     # -- state --------------------------------------------------------------
     def iteration(self):

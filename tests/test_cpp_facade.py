@@ -1,6 +1,8 @@
 """The C++ facade (include/exdyna/engine.hpp) a sparsim::Engine caller uses:
-compiles on CPU; on a GPU it replays the reference's hand-traced row
-(test_engine.cpp:79-131) through exdyna::Engine."""
+compiles on CPU (C++17 for the device-buffer API, C++20 for the
+GradientSource-driven Engine); on a GPU it replays the reference's
+hand-traced row (test_engine.cpp:79-131) through exdyna::Engine, both with
+device buffers and with a GradientSource."""
 import os
 import subprocess
 
@@ -9,28 +11,32 @@ import pytest
 from paper_2402_13781_b200._lib import LIB_PATH
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "tests", "cpp", "engine_facade_golden.cpp")
-EXE = os.path.join(ROOT, "paper_2402_13781_b200", "lib", "engine_facade_golden")
+CPP = os.path.join(ROOT, "tests", "cpp")
+LIBDIR = os.path.join(ROOT, "paper_2402_13781_b200", "lib")
+PROGS = {"engine_facade_golden": "c++17", "engine_source_golden": "c++20"}
 CUDA = "/usr/local/cuda"
 
 
-def _build():
+def _build(name):
     libdir = os.path.dirname(LIB_PATH)
-    subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"),
-                    "-I" + CUDA + "/include", SRC, "-o", EXE, "-L" + libdir, "-lexdyna",
+    exe = os.path.join(LIBDIR, name)
+    subprocess.run(["g++", "-std=" + PROGS[name], "-O2", "-Wall", "-Werror",
+                    "-I" + os.path.join(ROOT, "include"), "-I" + CUDA + "/include",
+                    os.path.join(CPP, name + ".cpp"), "-o", exe, "-L" + libdir, "-lexdyna",
                     "-L" + CUDA + "/lib64", "-lcudart", "-Wl,-rpath," + libdir,
                     "-Wl,-rpath," + CUDA + "/lib64"], check=True)
+    return exe
 
 
-def test_facade_compiles_and_links():
-    _build()
-    assert os.path.exists(EXE)
+@pytest.mark.parametrize("name", sorted(PROGS))
+def test_facade_compiles_and_links(name):
+    assert os.path.exists(_build(name))
 
 
 @pytest.mark.gpu
-def test_facade_hand_traced_row_on_gpu():
-    if not os.path.exists(EXE):
-        _build()
-    r = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
+@pytest.mark.parametrize("name", sorted(PROGS))
+def test_facade_on_gpu(name):
+    exe = _build(name)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout

@@ -77,3 +77,12 @@ def test_four_ranks_push_reduce_dense_and_sparse():
 def test_four_ranks_push_reduce_all_push():
     _run(4, "--sync", "p2p", "--steps", "12", port=29586, env={"EXD_HOLDER_SUM": "0"})
     _run(4, "--sync", "p2p", "--dtype", "f64", "--steps", "6", port=29587)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["nccl", "p2p"])
+def test_dead_peer_fails_the_step_instead_of_hanging(sync):
+    # NCCL path: async-error / timeout polling (EXD_NCCL_TIMEOUT_S); peer-memory
+    # path: the kernels' 20 s poll limit. Then the engine refuses further steps.
+    _run(2, "--sync", sync, "--kill-peer", "1", port=29588 if sync == "nccl" else 29589,
+         env={"EXD_NCCL_TIMEOUT_S": "5"})

@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p", "p2p-pull"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cap", type=float, default=None, help="max_density_cap")
+    ap.add_argument("--kill-peer", type=int, default=0,
+                    help="rank 1 stalls after 2 steps; rank 0's next steps must fail with the "
+                         "engine's collective error (EXD_ENCCL) instead of hanging")
     ap.add_argument("--inject", type=int, default=0,
                     help="perturb x on rank 1 after step 2; the next step must raise EngineError "
                          "(test_engine.cpp:219-226 across GPUs)")
@@ -59,6 +62,36 @@ def main():
         if rank == 0 else None
     tmp = torch.empty(args.n_g, dtype=tdt, device=f"cuda:{local}")
     ok = True
+    if args.kill_peer:
+        import time
+        for t in range(2):
+            src.gradient(t, rank, buf, args.dtype, eng.stream())
+            torch.cuda.synchronize()
+            eng.step([buf])
+        dist.barrier()
+        if rank != 0:
+            # a stalled peer: no further collectives from this rank until rank 0
+            # has given up (its peer-memory kernels poll for 20 s), then leave
+            # without a teardown barrier
+            time.sleep(40 if args.sync != "nccl" else 20)
+            os._exit(0)
+        t0 = time.time()
+        msgs = []
+        for t in range(2, 4):
+            src.gradient(t, rank, buf, args.dtype, eng.stream())
+            torch.cuda.synchronize()
+            try:
+                eng.step([buf])
+                msgs.append("no error")
+            except S.DeviceError as err:
+                msgs.append(str(err))
+        el = time.time() - t0
+        good = ("did not" in msgs[0] or "asynchronous error" in msgs[0]) and \
+            "engine unusable" in msgs[1] and el < 60
+        print(f"dist_check world={world} sync={args.sync} ({eng.sync_mode()}) kill-peer: "
+              f"{'PASS' if good else 'FAIL'} after {el:.1f} s: {msgs}", flush=True)
+        eng.close()
+        os._exit(0 if good else 1)
     if args.inject:
         msg = ""
         try:
