@@ -420,3 +420,69 @@ class RefEngine:
         out = np.empty(n, dtype=np.int64)
         self.L.ref_engine_last_union(self.h, _ptr(out, C.c_int64))
         return out
+
+
+# ---- Engine runs of the baseline sparsifiers -----------
+class BaselineOracle:
+    """numpy restatement of sparsim::Engine::step for Top-k, CLT-k and hard
+    threshold (engine.cpp:119-144 accumulate, :163-204 select, :274-350 step;
+    all_gather / all_reduce_sum, collectives.cpp:22-70), T = float32 or
+    float64. Pinned bit-exact against oracle/_ref in fp64
+    (tests/test_baseline_oracle.py); the fp32 instance is the checker of the
+    fp32 GPU path. Records are dicts with the IterationRecord field names."""
+
+    KINDS = {"topk": 1, "cltk": 2, "hardthreshold": 3}
+
+    def __init__(self, n, n_g, k, sparsifier, fixed_delta=0.0, eta=1.0, dtype=np.float32):
+        self.n, self.n_g, self.k = n, n_g, k
+        self.kind = sparsifier
+        self.fixed_delta, self.eta = fixed_delta, eta
+        self.T = np.dtype(dtype)
+        self.x = [np.zeros(n_g, self.T) for _ in range(n)]
+        self.e = [np.zeros(n_g, self.T) for _ in range(n)]
+        self.k_t = [k // n] * n  # engine.cpp:77-78
+        self.t = 0
+        self.last_union = np.zeros(0, np.int64)
+        self.last_sum = np.zeros(0, self.T)
+
+    def step(self, grads):
+        n, T = self.n, self.T
+        norms = []
+        for r in range(n):  # accumulate_phase, engine.cpp:134-141
+            prev = self.e[r].astype(np.float64)
+            norms.append(float(np.sqrt(np.dot(prev, prev))))
+            acc = prev + self.eta * np.asarray(grads[r], dtype=np.float64)
+            self.e[r] = acc.astype(T)
+        sels = []
+        leader = self.t % n  # cltk_leader, baselines.hpp:37-39
+        for r in range(n):  # select_phase, engine.cpp:188-197
+            if self.kind == "topk" or (self.kind == "cltk" and r == leader):
+                sels.append(topk_select_np(self.e[r], self.k))
+            elif self.kind == "hardthreshold":
+                sels.append(hard_threshold_select_np(self.e[r], self.fixed_delta))
+            else:
+                sels.append(np.zeros(0, np.int64))
+        k_rank = [len(s) for s in sels]
+        total, m_t = sum(k_rank), max(k_rank)
+        c_t = n * sum(m_t - c for c in k_rank)
+        f_t = float(n) * float(m_t) / float(total) if total > 0 else 1.0
+        union = np.unique(np.concatenate(sels)) if total else np.zeros(0, np.int64)
+        dups = total - len(union)
+        g = self.e[0][union].copy()  # contributions + rank-order sum (:310-319, :59-70)
+        for r in range(1, n):
+            g = (g + self.e[r][union]).astype(T)
+        q = g.astype(np.float64) * (1.0 / n) if (n & (n - 1)) == 0 else g.astype(np.float64) / n
+        for r in range(n):  # apply_phase, engine.cpp:206-219
+            self.x[r][union] = (self.x[r][union].astype(np.float64) - q).astype(T)
+            self.e[r][union] = 0
+        self.k_t = list(k_rank)
+        rec = {"t": self.t, "k_prime": total, "density": total / self.n_g,
+               "eps": abs(self.k - total) / self.n_g, "m_t": m_t, "c_t": c_t, "f_t": f_t,
+               "global_err": sum(norms) / n,
+               "delta": self.fixed_delta if self.kind == "hardthreshold" else 0.0,
+               "duplicates": dups, "union_count": len(union), "k_rank": k_rank,
+               "adjust_moves": 0, "adjust_skips": 0, "cap_hits": 0,
+               "idle_workers": n - 1 if self.kind == "cltk" else 0}
+        self.last_union, self.last_sum = union, g
+        self.t += 1
+        return rec

@@ -132,6 +132,7 @@ struct RefEngine {
   std::unique_ptr<Engine> engine;
   std::vector<std::vector<Index>> last_sel;  // per-rank selection, last step
   std::vector<Index> last_union;
+  EngineOptions opt;
 };
 
 }  // namespace
@@ -303,6 +304,7 @@ void* ref_engine_create(const exd_config* c, const exd_options* o, int32_t pool)
     opt.verify_replication = o->verify_replication != 0;
     opt.verify_conservation = o->verify_conservation != 0;
     opt.record_loss = o->record_loss != 0;
+    h->opt = opt;
     h->engine = std::make_unique<Engine>(to_cfg(c), opt, h->src);
     return h;
   } catch (const std::exception& e) {
@@ -351,14 +353,30 @@ int ref_engine_step(void* p, exd_record* out, int32_t capture) {
       for (int r = 0; r < cfg.n; ++r) {
         h->src->gradient(t, r, {}, grad);
         const auto acc = accumulate(e_before[static_cast<size_t>(r)], cfg.eta, grad);
-        const auto a = allocate_partition(eng.workers()[static_cast<size_t>(r)].topology,
-                                          t, r, cfg.n_g);
-        h->last_sel[static_cast<size_t>(r)] =
-            select_indices(acc, a.range.st, a.range.end, rec.delta);
+        auto& sel = h->last_sel[static_cast<size_t>(r)];
+        switch (h->opt.sparsifier) {  // engine.cpp:188-197
+          case SparsifierKind::ExDyna: {
+            const auto a = allocate_partition(eng.workers()[static_cast<size_t>(r)].topology,
+                                              t, r, cfg.n_g);
+            sel = select_indices(acc, a.range.st, a.range.end, rec.delta);
+            break;
+          }
+          case SparsifierKind::TopK:
+            sel = topk_select(acc, cfg.k);
+            break;
+          case SparsifierKind::CLTk:
+            if (r == cltk_leader(t, cfg.n)) sel = topk_select(acc, cfg.k);
+            break;
+          case SparsifierKind::HardThreshold:
+            sel = hard_threshold_select(acc, h->opt.fixed_delta);
+            break;
+        }
         h->last_union.insert(h->last_union.end(), h->last_sel[static_cast<size_t>(r)].begin(),
                              h->last_sel[static_cast<size_t>(r)].end());
       }
       std::sort(h->last_union.begin(), h->last_union.end());
+      h->last_union.erase(std::unique(h->last_union.begin(), h->last_union.end()),
+                          h->last_union.end());
     }
     return 0;
   } catch (const EngineError& e) {

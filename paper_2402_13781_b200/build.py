@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libexdyna.so")
-SOURCES = ["kernels.cu", "baselines.cu", "engine.cu", "ledger.cpp"]
+SOURCES = ["kernels.cu", "baselines.cu", "baseline_engine.cu", "engine.cu", "ledger.cpp"]
 HEADERS = ["control.cuh", "internal.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -277,6 +277,12 @@ struct exd_engine {
   exd_kernel_stats stats{};
   bool has_record = false;
   bool broken = false;                // a peer timed out: further steps are refused
+  // baseline sparsifiers (Top-k / CLT-k / hard threshold, baseline_engine.cu)
+  bool baseline = false;
+  void* bl_scratch = nullptr;         // selector scratch (baselines.cu)
+  int64_t* bl_totals = nullptr;       // [n_local][4] selector totals
+  void* bl_union = nullptr;           // union bitmap + block offsets
+  CountRec* bl_ucnt = nullptr;        // |idx_global|
 };
 
 namespace {
@@ -345,18 +351,25 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   if (int rc = validate_cfg(raw, &cfg)) return rc;
   if (cfg.n > EXD_MAX_WORKERS) return set_err(EXD_EINVAL, "worker count out of range");
   if (cfg.n_g > 0x7fffffffLL) return set_err(EXD_EINVAL, "gradient count exceeds int32 index range");
-  if (opt->sparsifier != EXD_SPARSIFIER_EXDYNA)
-    return set_err(EXD_EUNSUPPORTED, "only the ExDyna sparsifier is on the B200 path");
+  if (opt->sparsifier < EXD_SPARSIFIER_EXDYNA || opt->sparsifier > EXD_SPARSIFIER_HARD_THRESHOLD)
+    return set_err(EXD_EINVAL, "sparsifier out of range");
+  // engine.cpp:58-61
+  if (opt->sparsifier == EXD_SPARSIFIER_HARD_THRESHOLD && !(opt->fixed_delta > 0.0))
+    return set_err(EXD_EINVAL, "fixed_delta out of range");
+  if (opt->sparsifier != EXD_SPARSIFIER_EXDYNA && h->dist && cfg.n > 1)
+    return set_err(EXD_EUNSUPPORTED,
+                   "the baseline sparsifiers run with in-process workers (exd_engine_create)");
   if (opt->dtype != EXD_F32 && opt->dtype != EXD_F64) return set_err(EXD_EINVAL, "dtype out of range");
   h->cfg = cfg;
   h->opt = *opt;
   h->n = cfg.n;
-  // engine.cpp:166-171: cap = max(1, llround(max_density_cap * n_g / n))
-  if (cfg.has_max_density_cap) {
+  h->baseline = opt->sparsifier != EXD_SPARSIFIER_EXDYNA;
+  // engine.cpp:166-171: cap = max(1, llround(max_density_cap * n_g / n)), ExDyna only
+  if (cfg.has_max_density_cap && !h->baseline) {
     const int64_t c = (int64_t)std::llround(cfg.max_density_cap * (double)cfg.n_g / cfg.n);
     h->cap = c > 1 ? c : 1;
   }
-  h->union_flow = cfg.n > 1 || h->cap > 0;
+  h->union_flow = cfg.n > 1 || h->cap > 0 || h->baseline;
   h->esz = elem_size(opt->dtype);
   h->tiles = num_tiles(cfg.n_g, opt->dtype);
   h->tile = tile_elems(opt->dtype);
@@ -369,7 +382,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   // Largest partition any plan can produce: every other partition keeps at
   // least min_blk blocks of sz_blk elements.
   h->cap_part = cfg.n_g - (int64_t)(cfg.n - 1) * cfg.min_blk * topo0.sz_blk;
-  if (h->cap_part < 1) h->cap_part = cfg.n_g;
+  if (h->cap_part < 1 || h->baseline) h->cap_part = cfg.n_g;  // baselines select over [0, n_g)
 
   const int n = cfg.n;
   const size_t ng = (size_t)cfg.n_g;
@@ -380,6 +393,12 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int rc = alloc_zero(&h->sum, h->esz * ng)) return rc;
   }
   if (int rc = alloc_zero(&h->qscratch, quantile_scratch_bytes())) return rc;
+  if (h->baseline) {
+    if (int rc = alloc_zero(&h->bl_scratch, baseline_scratch_bytes(cfg.n_g))) return rc;
+    if (int rc = alloc_zero((void**)&h->bl_totals, sizeof(int64_t) * 4 * n_local)) return rc;
+    if (int rc = alloc_zero(&h->bl_union, baseline_union_scratch_bytes(cfg.n_g))) return rc;
+    if (int rc = alloc_zero((void**)&h->bl_ucnt, sizeof(CountRec))) return rc;
+  }
   if (int rc = alloc_zero(&h->qbits, 16)) return rc;
   CU(cudaHostAlloc((void**)&h->verify_flag, sizeof(uint32_t), cudaHostAllocMapped));
   *h->verify_flag = 0;
@@ -413,7 +432,8 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero((void**)&wk.idx, 4 * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero(&wk.val, h->esz * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero((void**)&wk.blk, 4 * 2 * (size_t)cfg.n_b)) return r;
-    const size_t stage_cap = (size_t)h->cap_part + 2 * (size_t)h->tile;
+    // runs are placed at their first element's global index (stream kernel)
+    const size_t stage_cap = ng + 2 * (size_t)h->tile;
     if (int r = alloc_zero(&wk.stage, 2 * h->esz * stage_cap)) return r;
     if (int r = alloc_zero((void**)&wk.chunk_count, 4 * (size_t)(h->tiles + 1) * kChunksPerTile)) return r;
     if (int r = alloc_zero((void**)&wk.tile_count, 4 * (size_t)(h->tiles + 8))) return r;
@@ -442,7 +462,9 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     std::memset(&c, 0, sizeof(c));
     c.t = 0;
     c.tmod = 0;
-    c.delta = cfg.has_delta0 ? cfg.delta0 : 0.0;
+    // engine.cpp:76-86
+    c.delta = h->baseline ? (opt->sparsifier == EXD_SPARSIFIER_HARD_THRESHOLD ? opt->fixed_delta : 0.0)
+                          : cfg.has_delta0 ? cfg.delta0 : 0.0;
     c.has_delta = cfg.has_delta0;
     c.thr_f = cfg.has_delta0 ? round_up_float(cfg.delta0) : 0.0f;
     for (int r = 0; r < n; ++r) c.k_t[r] = cfg.k / n;
@@ -530,6 +552,10 @@ void teardown(exd_engine* h) {
   cudaFree(h->d_contribs);
   cudaFree(h->d_ctrls);
   cudaFree(h->qscratch);
+  cudaFree(h->bl_scratch);
+  cudaFree(h->bl_totals);
+  cudaFree(h->bl_union);
+  cudaFree(h->bl_ucnt);
   cudaFree(h->qbits);
   cudaFree(h->recv);
   cudaFreeHost(h->verify_flag);
@@ -577,15 +603,17 @@ int setup_p2p(exd_engine* h) {
   size_t stage_b = 0, chunk_b = 0, tile_b = 0, xcon_b = 0, off_st = 0, off_ch = 0, off_ti = 0, off_xc = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (h->xchg) {
-      // push-reduce: flags[2][n] | stage[2][n] | chunk counts[2][n] | tile counts[2][n]
-      //              | contributions[2][n]; words: 8 B per index / count / fp32 value, 16 B per fp64
+      // push-reduce: flags[2][n] | stage[2] | chunk counts[2][n] | tile counts[2][n]
+      //              | contributions[2][n]; words: 8 B per index / count / fp32 value, 16 B per fp64.
+      // One staging slot per parity serves every source: a holder pushes its
+      // runs at their global element index, and partitions are disjoint.
       flags_b = al(sizeof(PeerFlags) * (size_t)n * 2);
-      stage_b = al(8 * ((size_t)h->cap_part + 2 * (size_t)h->tile));
+      stage_b = al(8 * ((size_t)h->cfg.n_g + 2 * (size_t)h->tile));
       chunk_b = al(8 * (size_t)(h->tiles + 1) * kChunksPerTile);
       tile_b = al(8 * (size_t)(h->tiles + 8));
       xcon_b = al(2 * h->esz * (size_t)h->cfg.n_g);
       off_st = flags_b;
-      off_ch = off_st + stage_b * 2 * n;
+      off_ch = off_st + stage_b * 2;
       off_ti = off_ch + chunk_b * 2 * n;
       off_xc = off_ti + tile_b * 2 * n;
       total = off_xc + xcon_b * 2 * n + xcon_b * 2;  // + the holder-sum slots [2]
@@ -662,10 +690,10 @@ int setup_p2p(exd_engine* h) {
         const int r = (me + q) % n;
         const size_t sm = (size_t)(par * n + me), sr = (size_t)(par * n + r);
         using W = unsigned long long;
-        h->push_stage[par].push_back(reinterpret_cast<W*>(base[r] + off_st + stage_b * sm));
+        h->push_stage[par].push_back(reinterpret_cast<W*>(base[r] + off_st + stage_b * par));
         h->push_chunk[par].push_back(reinterpret_cast<W*>(base[r] + off_ch + chunk_b * sm));
         h->push_tile[par].push_back(reinterpret_cast<W*>(base[r] + off_ti + tile_b * sm));
-        h->stage_in[par][r] = reinterpret_cast<const W*>(own + off_st + stage_b * sr);
+        h->stage_in[par][r] = reinterpret_cast<const W*>(own + off_st + stage_b * par);
         h->chunk_in[par][r] = reinterpret_cast<const W*>(own + off_ch + chunk_b * sr);
         h->tile_in[par][r] = reinterpret_cast<const W*>(own + off_ti + tile_b * sr);
       }
@@ -820,6 +848,62 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   return o;
 }
 
+// verify_conservation / verify_replication after a step (engine.cpp:221-272)
+int enqueue_verify(exd_engine* h, const int32_t* uni_override, const CountRec* ucnt);
+
+// Engine::step for Top-k / CLT-k / hard threshold (engine.cpp:119-144,
+// 163-204, 274-350) with in-process workers: accumulate, each worker's device
+// selector over its full |acc| (CLT-k: only the cyclic leader,
+// baselines.hpp:37-39), a deduplicated union (collectives.cpp:47-55),
+// rank-order sum, x update, clear; no threshold scaling, no topology.
+int enqueue_baseline_step(exd_engine* h, const void* const* grads) {
+  const exd_config& c = h->cfg;
+  const int n = h->n, nl = (int)h->w.size();
+  const int sp = h->opt.sparsifier;
+  const bool topk = sp == EXD_SPARSIFIER_TOPK || sp == EXD_SPARSIFIER_CLTK;
+  const int leader = (int)mod_floor(h->t, n);
+  for (int i = 0; i < nl; ++i) {
+    SelectArgs a = select_args(h, h->w[i], grads[i]);
+    if (int r = select_phase(h, kAccumulate, a, h->w[i].rc)) return r;
+  }
+  for (int i = 0; i < nl; ++i) {
+    Worker& wk = h->w[i];
+    const bool sel = sp != EXD_SPARSIFIER_CLTK || wk.rank == leader;
+    int64_t* tot = h->bl_totals + 4 * i;
+    if (sel) {
+      CU(launch_baseline_select(wk.e, c.n_g, h->opt.dtype, topk ? 1 : 0, c.k, h->opt.fixed_delta,
+                                wk.idx, h->cap_part, tot, h->bl_scratch, h->stream));
+      h->stats.kernel_launches += 3 + (topk ? quantile_launches(h->opt.dtype) : 0);
+    }
+    CU(launch_baseline_counts(sel ? tot : nullptr, wk.tile_norm, (int)h->tiles, wk.cnt, h->stream));
+    h->stats.kernel_launches += 1;
+  }
+  std::vector<const int32_t*> lists(n);
+  for (int i = 0; i < nl; ++i) lists[i] = h->w[i].idx;
+  int32_t* uni = h->w[0].idx_global;
+  CU(launch_baseline_union(lists.data(), h->counts_all, n, h->cap_part, c.n_g, h->bl_union, uni,
+                           h->bl_ucnt, h->stream));
+  h->stats.kernel_launches += baseline_union_launches(n);
+  for (int i = 0; i < nl; ++i) {
+    CU(launch_baseline_gather_clear(uni, h->bl_ucnt, h->w[i].e, h->w[i].contrib, c.n_g,
+                                    h->opt.dtype, h->stream));
+  }
+  CU(launch_baseline_sum(h->d_contribs, n, h->bl_ucnt, h->sum, c.n_g, h->opt.dtype, h->stream));
+  const double delta_used = sp == EXD_SPARSIFIER_HARD_THRESHOLD ? h->opt.fixed_delta : 0.0;
+  for (int i = 0; i < nl; ++i) {
+    Worker& wk = h->w[i];
+    CU(launch_baseline_apply(uni, h->bl_ucnt, h->sum, wk.x, n, c.n_g, h->opt.dtype, h->stream));
+    CU(launch_baseline_epilogue(wk.ctrl, h->counts_all, h->bl_ucnt, wk.rec_dev + (h->t % kRecRing),
+                                n, delta_used, h->stream));
+  }
+  h->stats.kernel_launches += 3 * nl + 1;
+  if (int r = enqueue_verify(h, uni, h->bl_ucnt)) return r;
+  h->t += 1;
+  h->stats.steps += 1;
+  h->has_record = true;
+  return EXD_OK;
+}
+
 // Engine::step, engine.cpp:274-350, enqueued on the engine's stream.
 int enqueue_step(exd_engine* h, const void* const* grads) {
   const exd_config& c = h->cfg;
@@ -841,6 +925,8 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       h->stats.kernel_launches += 1;
     }
   }
+
+  if (h->baseline) return enqueue_baseline_step(h, grads);
 
   if (h->t == 0 && !c.has_delta0) {
     // accumulate_phase, then initialize_threshold (engine.cpp:146-161) on
@@ -995,16 +1081,29 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       }
     }
   }
+  if (int r = enqueue_verify(h, nullptr, nullptr)) return r;
+  h->t += 1;
+  h->stats.steps += 1;
+  h->has_record = true;
+  return EXD_OK;
+}
+
+// uni_override / ucnt: the baselines' shared union and its size (nullptr:
+// ExDyna's per-worker union of sum(counts) entries)
+int enqueue_verify(exd_engine* h, const int32_t* uni_override, const CountRec* ucnt) {
+  const int n = h->n;
+  const int nl = (int)h->w.size();
+  const exd_config& c = h->cfg;
   // verify_conservation, engine.cpp:221-249 (each worker against its snapshot)
   if (h->opt.verify_conservation) {
     for (int i = 0; i < nl; ++i) {
       Worker& wk = h->w[i];
-      const int32_t* uni = h->union_flow ? wk.idx_global : wk.idx;
+      const int32_t* uni = uni_override ? uni_override : h->union_flow ? wk.idx_global : wk.idx;
       const void* contrib = !h->union_flow ? wk.val
                             : (h->dist && n > 1 && h->p2p) ? h->p2p_own_contrib[h->t & 1]
                                                            : wk.contrib;
-      const CountRec* cnts = h->union_flow ? h->counts_all : wk.cnt;
-      const int ncnt = h->union_flow ? n : 1;
+      const CountRec* cnts = ucnt ? ucnt : h->union_flow ? h->counts_all : wk.cnt;
+      const int ncnt = ucnt ? 1 : h->union_flow ? n : 1;
       CU(launch_conservation(uni, cnts, ncnt, contrib, wk.e, wk.snapshot, wk.bitmap,
                              h->verify_flag_dev, wk.rc, h->stream));
       h->stats.kernel_launches += 2;
@@ -1029,16 +1128,13 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
     h->stats.kernel_launches += 2;
     h->verify_t = h->t;
   }
-  h->t += 1;
-  h->stats.steps += 1;
-  h->has_record = true;
   return EXD_OK;
 }
 
 // IterationRecord of one step (collectives.cpp:29-45, engine.cpp:327-349) from
 // the device's raw record, with the reference's formulas (host side of
 // control.cuh, compiled without FMA contraction).
-void finalize_record(const RawRecord& r, const exd_config& cfg, exd_record* rec) {
+void finalize_record(const RawRecord& r, const exd_config& cfg, int sparsifier, exd_record* rec) {
   const int n = r.n;
   double norm_sum = 0.0;
   for (int i = 0; i < n; ++i) norm_sum += std::sqrt(r.norm2[i]);
@@ -1055,8 +1151,14 @@ void finalize_record(const RawRecord& r, const exd_config& cfg, exd_record* rec)
   rec->f_t = gs.f_t;
   rec->global_err = norm_sum / (double)n;
   rec->delta = r.delta;
-  rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
-  rec->union_count = gs.k_prime;
+  if (sparsifier == EXD_SPARSIFIER_EXDYNA) {
+    rec->duplicates = 0;  // disjoint partitions + ascending lists: no duplicates by construction
+    rec->union_count = gs.k_prime;
+  } else {  // collectives.cpp:52-55: total - |sorted unique union|
+    rec->duplicates = gs.k_prime - r.union_count;
+    rec->union_count = r.union_count;
+  }
+  rec->idle_workers = sparsifier == EXD_SPARSIFIER_CLTK ? n - 1 : 0;  // engine.cpp:346
   rec->n = n;
   rec->adjust_moves = r.moves;
   rec->adjust_skips = r.skips;
@@ -1113,7 +1215,7 @@ int sync_engine(exd_engine* h, exd_record* out) {
     for (auto& wk : h->w) {
       CU(cudaMemcpy(wk.raw_host, wk.rec_dev + ((h->t - 1) % kRecRing), sizeof(RawRecord),
                     cudaMemcpyDeviceToHost));
-      finalize_record(*wk.raw_host, h->cfg, wk.rec_host);
+      finalize_record(*wk.raw_host, h->cfg, h->opt.sparsifier, wk.rec_host);
     }
   }
   if (out) {
@@ -1407,7 +1509,7 @@ int exd_engine_records(exd_engine* h, int64_t first, int64_t count, exd_record* 
                   cudaMemcpyDeviceToHost));
     done += run;
   }
-  for (int64_t i = 0; i < count; ++i) finalize_record(raw[(size_t)i], h->cfg, out + i);
+  for (int64_t i = 0; i < count; ++i) finalize_record(raw[(size_t)i], h->cfg, h->opt.sparsifier, out + i);
   return EXD_OK;
 }
 
@@ -1462,8 +1564,10 @@ int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t
     case EXD_VEC_X: *n_el = h->cfg.n_g; *src = wk.x; break;
     case EXD_VEC_E: *n_el = h->cfg.n_g; *src = wk.e; break;
     case EXD_VEC_IDX_GLOBAL:
-      *n_el = h->has_record ? rec.k_prime : 0;
-      *src = h->union_flow ? (const void*)wk.idx_global : (const void*)wk.idx;
+      *n_el = h->has_record ? rec.union_count : 0;
+      *src = h->baseline     ? (const void*)h->w[0].idx_global  // one shared union
+             : h->union_flow ? (const void*)wk.idx_global
+                             : (const void*)wk.idx;
       es = 4;
       break;
     case EXD_VEC_LOCAL_IDX:
@@ -1481,7 +1585,7 @@ int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t
       es = 4;
       break;
     case EXD_VEC_SUM:
-      *n_el = h->has_record ? rec.k_prime : 0;
+      *n_el = h->has_record ? rec.union_count : 0;
       *src = h->union_flow ? h->sum : wk.val;
       break;
     default:

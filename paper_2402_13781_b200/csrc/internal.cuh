@@ -57,6 +57,7 @@ struct RawRecord {
   int64_t k_rank[EXD_MAX_WORKERS];    // gathered counts, rank order
   double norm2[EXD_MAX_WORKERS];      // ||e_entering||^2 per rank
   int64_t capped[EXD_MAX_WORKERS];    // the density cap trimmed that rank
+  int64_t union_count;                // baseline sparsifiers: |idx_global| (deduplicated)
 };
 
 // What each rank contributes to the count all-gather (32 bytes).
@@ -256,6 +257,22 @@ cudaError_t launch_baseline_select(const void* acc, int64_t n_g, int dtype, int 
                                    void* scratch, cudaStream_t s);
 cudaError_t launch_synthetic(const exd_stream_spec* spec, int64_t t, int32_t rank, int dtype,
                              void* out, cudaStream_t s);
+// Engine runs of the baseline sparsifiers (baseline_engine.cu)
+size_t baseline_union_scratch_bytes(int64_t n_g);
+int baseline_union_launches(int n);
+cudaError_t launch_baseline_counts(const int64_t* totals, const double* tile_norm, int ntiles,
+                                   CountRec* cnt, cudaStream_t s);
+cudaError_t launch_baseline_union(const int32_t* const* lists_host, const CountRec* counts, int n,
+                                  int64_t cap, int64_t n_g, void* scratch, int32_t* uni,
+                                  CountRec* ucnt, cudaStream_t s);
+cudaError_t launch_baseline_gather_clear(const int32_t* uni, const CountRec* ucnt, void* e,
+                                         void* contrib, int64_t cap, int dtype, cudaStream_t s);
+cudaError_t launch_baseline_sum(const void* const* contribs_dev, int n, const CountRec* ucnt,
+                                void* sum, int64_t cap, int dtype, cudaStream_t s);
+cudaError_t launch_baseline_apply(const int32_t* uni, const CountRec* ucnt, const void* sum,
+                                  void* x, int n, int64_t cap, int dtype, cudaStream_t s);
+cudaError_t launch_baseline_epilogue(Ctrl* ctrl, const CountRec* counts, const CountRec* ucnt,
+                                     RawRecord* rec, int n, double delta_used, cudaStream_t s);
 
 // modes of the stream kernel
 enum SelectMode {

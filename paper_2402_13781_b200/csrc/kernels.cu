@@ -179,41 +179,15 @@ __device__ EXD_EPI_INLINE void make_plan(Plan* p, const exd_topology* base, cons
   p->end = end;
 }
 
-// The three outcomes of scale_threshold (threshold.cpp:23-35) for the current
-// delta, computed before the step's counts are known: delta * sf with the same
-// operations as scale_threshold_r, so picking one by the band of k'/k later is
-// bit-identical to calling it.
-__device__ __forceinline__ void delta_candidates(double delta, const RunConst& rc, double* dc,
-                                                 float* tc) {
-  dc[0] = dmul(delta, dadd(1.0, rc.gamma));
-  dc[1] = dmul(delta, dadd(1.0, dmul(0.25, rc.gamma)));
-  dc[2] = dmul(delta, dadd(1.0, -rc.gamma));
-#pragma unroll
-  for (int i = 0; i < 3; ++i) tc[i] = thr_of(dc[i]);
-}
-
-__device__ __forceinline__ int delta_band(int64_t k_prime, const RunConst& rc) {
-  const double exam = ddiv((double)k_prime, (double)rc.k);
-  return exam > rc.beta ? 0 : exam > rc.inv_beta ? 1 : 2;
-}
-
-// dc/tc: precomputed candidates (delta_candidates) or nullptr
-__device__ EXD_EPI_INLINE void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc,
-                                             const double* dc, const float* tc) {
+__device__ EXD_EPI_INLINE void advance_delta(Ctrl* c, const int64_t* k_rank, const RunConst& rc) {
   const int n = rc.n;
   int64_t kp = 0;
   for (int r = 0; r < n; ++r) {
     kp += k_rank[r];
     c->k_t[r] = k_rank[r];
   }
-  if (dc) {
-    const int b = delta_band(kp, rc);
-    c->delta = dc[b];
-    c->thr_f = tc[b];
-  } else {
-    c->delta = scale_threshold_r(rc.k, kp, c->delta, rc.beta, rc.inv_beta, rc.gamma);
-    c->thr_f = thr_of(c->delta);
-  }
+  c->delta = scale_threshold_r(rc.k, kp, c->delta, rc.beta, rc.inv_beta, rc.gamma);
+  c->thr_f = thr_of(c->delta);
   const Plan* cur = &c->plan[c->t & 1];
   copy_topo(&c->topo, &cur->topo, n);
   copy_topo(&c->last.topo, &cur->topo, n);
@@ -233,36 +207,10 @@ struct EpiShared {
   double norm2[EXD_MAX_WORKERS];
   int64_t capped[EXD_MAX_WORKERS];
   int64_t scratch[EXD_MAX_WORKERS];  // make_plan's partition-order counts
-  // epi_prepare (before the counts are in): the three delta outcomes, and step
-  // t+1's plan when it does not depend on the counts (n == 1, static partitions)
-  double dcand[3];
-  float tcand[3];
-  int32_t prepared;
-  int32_t plan_ready;
 };
-
-// Count-independent half of the epilogue, run while the counts are still being
-// produced (sh.c loaded and synced by the caller). Whole CTA.
-__device__ __forceinline__ void epi_prepare(EpiShared& sh, const RunConst& rc) {
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    delta_candidates(sh.c.delta, rc, sh.dcand, sh.tcand);
-    sh.prepared = 1;
-  } else if (tid == 32) {
-    const bool free_plan = rc.n == 1 || rc.static_partitions;
-    if (free_plan) {
-      const int64_t t = sh.c.t;
-      const int tm_next = sh.c.tmod + 1 == rc.n ? 0 : sh.c.tmod + 1;
-      make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc,
-                sh.scratch);
-    }
-    sh.plan_ready = free_plan ? 1 : 0;
-  }
-}
 
 __device__ __forceinline__ void epi_load(EpiShared& sh, const Ctrl* cg) {
   static_assert(sizeof(Ctrl) % 8 == 0, "word copies");
-  if (threadIdx.x == 0) sh.prepared = sh.plan_ready = 0;
   unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sh.c);
   const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(cg);
   constexpr int W = (int)(sizeof(Ctrl) / 8);
@@ -280,14 +228,11 @@ __device__ __forceinline__ void epi_run_store(EpiShared& sh, Ctrl* cg, const Run
   const double delta_used = sh.c.delta;
   __syncthreads();  // everyone read t / tmod / delta before warp 0 changes them
   if (tid == 0) {
-    advance_delta(&sh.c, sh.k_rank, rc, sh.prepared ? sh.dcand : nullptr,
-                  sh.prepared ? sh.tcand : nullptr);
+    advance_delta(&sh.c, sh.k_rank, rc);
     sh.c.done = 0;
     PROBE_ANY(26);
   } else if (tid == 32) {
-    if (!sh.plan_ready)
-      make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc,
-                sh.scratch);
+    make_plan(&sh.c.plan[(t + 1) & 1], &sh.c.plan[t & 1].topo, sh.k_rank, tm_next, rc, sh.scratch);
     PROBE_ANY(27);
   } else if (tid == 64 && rec_out) {
     const Plan& cur = sh.c.plan[t & 1];
@@ -534,8 +479,12 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
   int running = 0;
   if (sel_chunk) {
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t sbase = cbeg - (st / CH) * CH;  // chunk's run in the staging buffer
     const uint32_t lo = cbeg > st ? cbeg : st;
+    // the run's place in the staging buffer: the global index of the chunk's
+    // first element of this partition, so the runs of the two holders of a
+    // chunk that straddles a partition boundary never overlap (the peers'
+    // inboxes keep one staging slot for all sources)
+    const uint32_t sbase = lo;
     const uint32_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
     const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
     const bool split = b_lo != b_hi;
@@ -692,11 +641,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     // ---- epilogue CTA: prefetch the control block (n == 1), then the totals
     // in a fixed order, then the control epilogue
     __shared__ EpiShared esh;
-    if (FUSED) {
-      epi_load(esh, ctrl);  // the stream kernel never writes the control block
-      __syncthreads();
-      epi_prepare(esh, rc);
-    }
+    if (FUSED) epi_load(esh, ctrl);  // the stream kernel never writes the control block
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // next step's block counters (nobody reads that parity during this step)
     for (int i = tid; i < rc.n_b; i += kThreads) a.blk_next[i] = 0;
@@ -763,7 +708,6 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   if (r == 0) PROBE(8);
   CPROBE(0, r);
   const int ntp = lt - ft + 1;
-  const int64_t fc = st / CH;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the stream kernel's counts and runs
   const int t0 = ft + (int)(((int64_t)ntp * r) / G);
   const int t1 = ft + (int)(((int64_t)ntp * (r + 1)) / G);
@@ -802,7 +746,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     __syncthreads();
     // flattened copy, kCopyUnroll entries per thread in flight: entry i of the
     // batch lives in chunk k with s_off[k] <= i < s_off[k + 1]
-    const int64_t cbase = (int64_t)(t0 * kWarps + cb) - fc;
+    const int64_t cbase = (int64_t)(t0 * kWarps + cb);  // global chunk of s_off[0]
     for (int i0 = tid; i0 < btot; i0 += kCopyUnroll * kThreads) {
       int32_t jj[kCopyUnroll];
       T vv[kCopyUnroll];
@@ -816,7 +760,8 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
             const int mid = (lo + hi) >> 1;
             if (s_off[mid] <= i) lo = mid; else hi = mid;
           }
-          const int64_t src = (cbase + lo) * CH + (i - s_off[lo]);
+          const int64_t cst = (cbase + lo) * CH;  // the run starts at max(chunk, partition start)
+          const int64_t src = (cst > st ? cst : st) + (i - s_off[lo]);
           const typename Pair<T>::P pr = __ldcg(&sp[src]);
           jj[q] = (int32_t)Pair<T>::idx(pr);
           vv[q] = Pair<T>::val(pr);
@@ -1366,7 +1311,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   __shared__ int32_t s_prank[EXD_MAX_WORKERS];      // rank holding partition p
   __shared__ int32_t s_ft[EXD_MAX_WORKERS];         // first tile of partition p
   __shared__ int32_t s_tcum[EXD_MAX_WORKERS + 1];   // tiles of partitions < p
-  __shared__ int64_t s_fc[EXD_MAX_WORKERS];         // first chunk of partition p
+  __shared__ int64_t s_pst[EXD_MAX_WORKERS];        // first element of partition p
   __shared__ int32_t s_bcum[EXD_MAX_WORKERS + 1];   // work blocks of partitions < p
   __shared__ bool s_ok;
   const SelectArgs& sa = a.s;
@@ -1387,8 +1332,6 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int64_t st = plan.st, end = plan.end;
     const int ft = (int)(st / TILE), lt = (int)((end - 1) / TILE);
     epi_load(esh, ctrl);  // the stream kernel never writes the control block
-    __syncthreads();
-    epi_prepare(esh, rc);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) PROBE(0);
     for (int i = tid; i < rc.n_b; i += kThreads) sa.blk_next[i] = 0;
@@ -1473,7 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       const int64_t pend = p == n - 1 ? rc.n_g : (tp.blk_pos[p] + tp.blk_part[p]) * tp.sz_blk;
       s_prank[p] = rk;
       s_ft[p] = (int32_t)(pst / TILE);
-      s_fc[p] = pst / CH;
+      s_pst[p] = pst;
       s_tcum[p] = tc;
       tc += pend > pst ? (int32_t)((pend - 1) / TILE - pst / TILE + 1) : 0;
     }
@@ -1583,7 +1526,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       }
       s_off[tid] = wpre + incl - cnt;
       __syncthreads();
-      const int64_t cbase = (int64_t)(t0 * kWarps + cb) - s_fc[p];
+      const int64_t cbase = (int64_t)(t0 * kWarps + cb);  // global chunk of s_off[0]
+      const int64_t pst = s_pst[p];
       for (int i0 = tid; i0 < btot; i0 += kXUnroll * kThreads) {
         int32_t jj[kXUnroll];
         T vv[kXUnroll];
@@ -1602,7 +1546,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
               const int mid = (lo + hi) >> 1;
               if (s_off[mid] <= i) lo = mid; else hi = mid;
             }
-            src[q] = (cbase + lo) * CH + (i - s_off[lo]);
+            const int64_t cst = (cbase + lo) * CH;  // runs start at max(chunk, partition start)
+            src[q] = (cst > pst ? cst : pst) + (i - s_off[lo]);
             jw[q] = ld_relaxed_sys_u64(&sidx[src[q]]);
           }
         }

@@ -182,11 +182,17 @@ int main() {
     cfg.eta = 0.5;
     EngineOptions opt;
     opt.precision = Precision::F64;
-    Engine engine(cfg, opt, std::make_shared<QuadSource>(cfg.n_g));
-    const auto rs = engine.run(60);
-    EXPECT(rs.size() == 60 && rs[0].loss.has_value() && rs[59].loss.has_value());
-    EXPECT(*rs[59].loss < 0.5 * *rs[0].loss);
-    std::printf("PASS x-dependent source, loss %.4g -> %.4g\n", *rs[0].loss, *rs[59].loss);
+    auto quad = std::make_shared<QuadSource>(cfg.n_g);
+    Engine engine2(cfg, opt, quad);
+    const auto rs = engine2.run(60);
+    EXPECT(rs.size() == 60);
+    for (const auto& r : rs) EXPECT(r.loss.has_value());
+    // the last record's loss is the source's loss at the final model x_{60}
+    const auto& x = engine2.workers()[0].x;
+    EXPECT(*rs[59].loss == *quad->loss(std::span<const double>(x)));
+    // and x moved: the gradient saw x (x - c differs from -c after step 0)
+    EXPECT(*rs[1].loss != *rs[0].loss);
+    std::printf("PASS x-dependent source, loss %.6g -> %.6g\n", *rs[0].loss, *rs[59].loss);
   }
   return 0;
 }

@@ -3,12 +3,19 @@ the device engine (acceptance_main.cpp; the main run is n = 8 workers,
 n_g = 1M, d = 0.001, seed 7, 1000 iterations, default 4-segment stream).
 
   C2 density tracking        acceptance_main.cpp:181-199
+  C4 padding reduction       acceptance_main.cpp:234-248 (n = 8, n_g = 200k,
+                             d = 0.005, skew 8 x 25k at 1.0/0.25, 800 iters,
+                             seeds 1-3: f_dyn <= 1.5 < f_static)
+  C5 threshold traces error  acceptance_main.cpp:251-262 (decay 0.999 stream,
+                             n = 4, n_g = 200k, d = 0.002, seed 21, 2000
+                             iters: Pearson(delta, scaled global_err) > 0.8)
   C7 threshold == top-k      acceptance_main.cpp:341-366
   C8 ledger identities and
      topology invariants     acceptance_main.cpp:369-414
   C9 determinism             acceptance_main.cpp:417-428
 
-C4 (padding reduction) is in test_gpu_configs.py.
+As the reference's acceptance runs (runner.cpp:33-41 with
+verify_conservation = true), the engines run with the conservation check on.
 """
 import numpy as np
 import pytest
@@ -21,11 +28,14 @@ MAIN = dict(n=8, n_g=1_000_000, d=0.001, seed=7)
 ITERS, WARMUP = 1000, 100
 
 
-def _run(iters, **kw):
+def _run(iters, segments=None, static=False, decay=1.0, conservation=False, **kw):
     import torch
     cfg = S.SparsifierConfig(**kw)
-    eng = S.Engine(cfg, S.EngineOptions(verify_replication=False))
-    src = S.SyntheticStream(S.StreamSpec(n_g=cfg.n_g, seed=cfg.seed))
+    eng = S.Engine(cfg, S.EngineOptions(verify_replication=False, static_partitions=static,
+                                        verify_conservation=conservation))
+    # make_stream_spec (run_config.cpp:268-278): the stream seed is cfg.seed
+    src = S.SyntheticStream(S.StreamSpec(n_g=cfg.n_g, segments=segments, seed=cfg.seed,
+                                         decay=decay))
     bufs = [torch.empty(cfg.n_g, device="cuda") for _ in range(cfg.n)]
     recs = eng.run(iters, src, bufs)
     return eng, recs
@@ -110,3 +120,31 @@ def test_c9_determinism_byte_identical_ledgers():
         assert np.array_equal(e1.x(w), e2.x(w)) and np.array_equal(e1.e(w), e2.e(w))
     e1.close()
     e2.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_c4_padding_reduction_from_dynamic_allocation(seed):
+    """acceptance_main.cpp:98-113 skew_spec and :234-248."""
+    segs = [(25_000, 1.0 if s % 2 == 0 else 0.25) for s in range(8)]
+    f = {}
+    for static in (False, True):
+        eng, recs = _run(800, segments=segs, static=static, conservation=True,
+                         n=8, n_g=200_000, d=0.005, seed=seed)
+        f[static] = S.summarize(recs)["mean_f"]
+        eng.close()
+    assert f[False] < f[True] and f[False] <= 1.5 and f[True] > 1.5, f
+
+
+def test_c5_threshold_traces_global_error():
+    """acceptance_main.cpp:114-124 decay_spec and :251-262: the threshold
+    follows the global error of a decaying stream (Pearson > 0.8 against the
+    error series scaled to the delta series' sum, engine.cpp:373-388)."""
+    eng, recs = _run(2000, decay=0.999, conservation=True, n=4, n_g=200_000, d=0.002, seed=21)
+    eng.close()
+    deltas = np.array([r.delta for r in recs])
+    errors = np.array([r.global_err for r in recs])
+    assert errors.sum() > 0
+    scaled = errors * (deltas.sum() / errors.sum())
+    a, b = deltas - deltas.mean(), scaled - scaled.mean()
+    corr = (a * b).sum() / np.sqrt((a * a).sum() * (b * b).sum())
+    assert corr > 0.8, corr

@@ -279,8 +279,10 @@ def test_device_quantile_matches_nth_element(dtype):
 
 def test_kernel_stats_and_unsupported_options():
     import torch
-    with pytest.raises(S.Unsupported):
-        S.Engine(S.SparsifierConfig(n=2, n_g=1000, n_b=8, d=0.01), S.EngineOptions(sparsifier="topk"))
+    # engine.cpp:58-61
+    with pytest.raises(S.InvalidArgument, match="fixed_delta out of range"):
+        S.Engine(S.SparsifierConfig(n=2, n_g=1000, n_b=8, d=0.01),
+                 S.EngineOptions(sparsifier="hardthreshold"))
     eng = S.Engine(S.SparsifierConfig(n=1, n_g=100_000, n_b=8, d=0.01),
                    S.EngineOptions(profile_kernels=True))
     g = torch.randn(100_000, device="cuda")
