@@ -712,6 +712,11 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   const int t0 = ft + (int)(((int64_t)ntp * r) / G);
   const int t1 = ft + (int)(((int64_t)ntp * (r + 1)) / G);
   const int nch = (t1 - t0) * kWarps;
+  T* __restrict__ val = static_cast<T*>(a.val);
+  T* __restrict__ x = static_cast<T*>(a.x);
+  int32_t* __restrict__ idx = a.idx;
+  using P = typename Pair<T>::P;
+  const P* __restrict__ sp = static_cast<const P*>(a.stage);
   // the chunk counts do not depend on the base: load them in the same round trip
   int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
   const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
@@ -719,10 +724,6 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   if (r == G - 1) PROBE(10);
   CPROBE(1, r);
 
-  T* __restrict__ val = static_cast<T*>(a.val);
-  T* __restrict__ x = static_cast<T*>(a.x);
-  int32_t* __restrict__ idx = a.idx;
-  const typename Pair<T>::P* __restrict__ sp = static_cast<const typename Pair<T>::P*>(a.stage);
   int64_t running = base;
   for (int cb = 0; cb < nch; cb += kThreads) {
     const int nb = nch - cb < kThreads ? nch - cb : kThreads;
