@@ -206,6 +206,7 @@ struct Worker {
   exd_record* rec_host = nullptr;     // pinned: last record copied back at sync
   RawRecord* rec_dev = nullptr;       // device ring of kRecRing raw records (slot t % kRecRing)
   RawRecord* raw_host = nullptr;      // pinned: last raw record copied back at sync
+  unsigned long long* range_words = nullptr;  // finish kernel, large vectors ([3][kMaxCtas])
   Plan plan0{};                       // host copy of the t = 0 plan
 };
 
@@ -250,6 +251,7 @@ struct exd_engine {
   unsigned int* p2p_err = nullptr;    // pinned host copy
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
+  unsigned long long* xrange_words = nullptr;  // push-reduce, large vectors: [3][kMaxCtas]
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
   //   | chunk counts[2][n] | tile counts[2][n] | contrib[2][n][n_g]   ([2]: step parity;
@@ -439,6 +441,10 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero((void**)&wk.tile_count, 4 * (size_t)(h->tiles + 8))) return r;
     if (int r = alloc_zero((void**)&wk.tile_norm, 8 * (size_t)(h->tiles + 1))) return r;
     if (int r = alloc_zero((void**)&wk.ctrl, sizeof(Ctrl))) return r;
+    // more tiles than one round of the finish kernel's base sum: published range words
+    if (h->tiles > kBaseRoundTiles)
+      if (int r = alloc_zero((void**)&wk.range_words, sizeof(unsigned long long) * 3 * kMaxCtas))
+        return r;
     if (opt->verify_conservation) {
       if (int r = alloc_zero(&wk.snapshot, h->esz * ng)) return r;
       if (int r = alloc_zero((void**)&wk.bitmap, 4 * ((ng + 31) / 32))) return r;
@@ -524,6 +530,7 @@ void teardown(exd_engine* h) {
   cudaFreeHost(h->p2p_err);
   cudaFree(h->p2p_err_dev);
   cudaFree(h->p2p_gate);
+  cudaFree(h->xrange_words);
   for (auto& wk : h->w) {
     cudaFree(wk.x);
     cudaFree(wk.e);
@@ -535,6 +542,7 @@ void teardown(exd_engine* h) {
     cudaFree(wk.tile_count);
     cudaFree(wk.tile_norm);
     cudaFree(wk.ctrl);
+    cudaFree(wk.range_words);
     cudaFree(wk.idx_global);
     cudaFree(wk.contrib);
     cudaFree(wk.grad_stage);
@@ -739,6 +747,9 @@ int setup_p2p(exd_engine* h) {
   *h->p2p_err = 0;
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
   if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
+  if (h->xchg && h->tiles > kBaseRoundTiles)
+    if (int r2 = alloc_zero((void**)&h->xrange_words, sizeof(unsigned long long) * 3 * kMaxCtas))
+      return r2;
   // barrier: every rank has mapped every peer before anyone steps
   int* d_b = nullptr;
   CU(cudaMalloc((void**)&d_b, sizeof(int)));
@@ -808,6 +819,7 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.k1_npush = h->xchg ? h->n : 0;  // every peer, then this rank's own inbox
   // pairs of ~2k/n selections (16 B fp64, 8 B fp32) against a 32 MB share of L2
   a.stage_keep = 2 * (double)h->cfg.k / h->n * (h->esz == 8 ? 16 : 8) < 32e6 ? 1 : 0;
+  a.range_words = wk.range_words;
   const int par = (int)(h->t & 1);  // this step's parity slots
   for (int q = 0; q < a.k1_npush; ++q) {
     a.push_stage[q] = h->push_stage[par][q];
@@ -845,6 +857,7 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   o.epoch = (unsigned long long)h->t + 1;
   o.err = h->p2p_err_dev;
   o.me = wk.rank;
+  o.xrange_words = h->xrange_words;
   return o;
 }
 

@@ -110,12 +110,15 @@ struct SelectArgs {
   unsigned long long* push_chunk[EXD_MAX_WORKERS];  // [k1_npush] my per-chunk count slot
   unsigned long long* push_tile[EXD_MAX_WORKERS];   // [k1_npush] my per-tile count slot
   int32_t k1_npush;             // 0: no pushes
+  unsigned long long* range_words;  // finish kernel, large vectors: [3][kMaxCtas] published
+                                    // range counts / ||e||^2 halves (nullptr: small vector)
   int32_t stage_keep;           // staged pairs small enough to keep in L2 (evict_last);
                                 // else streamed (evict_first) so they do not crowd the
                                 // 126 MB L2 at large k
 };
 
 constexpr int kMaxCtas = 2048;
+constexpr int kBaseRoundTiles = 3072;  // tiles one round of the finish kernel's base sum covers
 constexpr int kChunksPerTile = 8;  // one warp chunk per warp of the stream kernel
 
 // union build + contribution gather + residual clear (K4 + K5)
@@ -207,6 +210,9 @@ struct ExchangeArgs {
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
   int32_t me;
+  unsigned long long* xrange_words;  // large vectors: [3][kMaxCtas] work blocks' range counts
+                                     // and ||e||^2 halves as {payload, epoch} words
+                                     // (nullptr: small vector)
 };
 
 // kernel launchers (kernels.cu)

@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
 // Everything is latency-bound here, so every phase issues its loads wide and
 // independent before using them.
 constexpr int kSumUnroll = 12;
+static_assert(kSumUnroll * kThreads == kBaseRoundTiles, "engine.cu sizes the range words by this");
 
 // sum of cnt[lo, hi) (int32) by the whole CTA: kSumUnroll independent loads per
 // thread per round (one round covers 3072 tiles)
@@ -607,6 +608,42 @@ __device__ __forceinline__ int64_t cta_sum_counts(const int32_t* __restrict__ cn
   return t;
 }
 
+// Large vectors (more tiles than one round of cta_sum_counts covers): every
+// copy CTA publishes, as {payload, epoch} words (no fences: an aligned 8-byte
+// word is single-copy atomic), the selection count of its tile range and the
+// two halves of an ||e||^2 partial over an equal slice of ALL tiles; a CTA's
+// base is then the sum of the earlier CTAs' range words and the epilogue CTA
+// totals G words, instead of rounds over every tile count before it. All
+// finish CTAs are resident (<= 4 per SM by registers, the grid is 3 per SM + 1),
+// so the polls cannot deadlock; the words are read only within this launch.
+struct RangeWords {
+  unsigned long long* sum;   // [G] selected in the CTA's tile range
+  unsigned long long* nlo;   // [G] low / high 32 bits of the ||e||^2 partial
+  unsigned long long* nhi;
+};
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
+}
+
+// sum of words w[0, m) carrying epoch ep (polled), by the whole CTA
+__device__ int64_t cta_sum_words(const unsigned long long* w, int m, uint32_t ep, int64_t* red) {
+  int64_t s = 0;
+  for (int i = threadIdx.x; i < m; i += kThreads) {
+    unsigned long long v;
+    while ((uint32_t)((v = ld_volatile_u64(&w[i])) >> 32) != ep) __nanosleep(32);
+    s += (uint32_t)v;
+  }
+  s = warp_sum(s);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  int64_t t = 0;
+#pragma unroll
+  for (int q = 0; q < kWarps; ++q) t += red[q];
+  return t;
+}
+
 #ifndef EXD_COPY_UNROLL
 #define EXD_COPY_UNROLL 8
 #endif
@@ -615,7 +652,7 @@ __device__ __forceinline__ int64_t cta_sum_counts(const int32_t* __restrict__ cn
 #endif
 constexpr int kCopyUnroll = EXD_COPY_UNROLL;  // staged entries in flight per thread
 
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool BIG>
 __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst rc) {
   constexpr int CH = chunk_of<T>();
   constexpr int TILE = tile_of<T>();
@@ -649,7 +686,20 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     const int nt = (int)((n_g + TILE - 1) / TILE);
     double pn = 0.0;
     int64_t pk = 0;
-    for (int i = tid; i < nt; i += kSumUnroll * kThreads) {
+    if (BIG) {  // large vector: the copy CTAs' published partials
+      const RangeWords rw{a.range_words, a.range_words + kMaxCtas, a.range_words + 2 * kMaxCtas};
+      const uint32_t ep = (uint32_t)(a.t + 1);
+      // fixed order: thread i takes CTAs i, i + 256, ... in turn
+      for (int q = tid; q < G; q += kThreads) {
+        unsigned long long s_, lo, hi;
+        while ((uint32_t)((s_ = ld_volatile_u64(&rw.sum[q])) >> 32) != ep) __nanosleep(32);
+        while ((uint32_t)((lo = ld_volatile_u64(&rw.nlo[q])) >> 32) != ep) __nanosleep(32);
+        while ((uint32_t)((hi = ld_volatile_u64(&rw.nhi[q])) >> 32) != ep) __nanosleep(32);
+        pk += (uint32_t)s_;
+        pn += __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+      }
+    }
+    for (int i = tid; i < (BIG ? 0 : nt); i += kSumUnroll * kThreads) {
       double v[kSumUnroll];
       int c[kSumUnroll];
 #pragma unroll
@@ -719,7 +769,33 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   const P* __restrict__ sp = static_cast<const P*>(a.stage);
   // the chunk counts do not depend on the base: load them in the same round trip
   int cnt = tid < nch ? __ldcg(&a.chunk_count[t0 * kWarps + tid]) : 0;
-  const int64_t base = cta_sum_counts(a.tile_count, ft, t0, s_red);
+  int64_t base;
+  if (BIG) {
+    // own range count and the ||e||^2 partial of an equal slice of all tiles,
+    // published; the base from the earlier CTAs' words
+    const int nt = (int)((n_g + TILE - 1) / TILE);
+    const int n0 = (int)(((int64_t)nt * r) / G), n1 = (int)(((int64_t)nt * (r + 1)) / G);
+    double pn = 0.0;
+    for (int i = n0 + tid; i < n1; i += kThreads) pn += __ldcg(&a.tile_norm[i]);
+    const int64_t mine = cta_sum_counts(a.tile_count, t0, t1, s_red);
+    pn = warp_sum(pn);
+    if (lane == 0) s_dred[warp] = pn;
+    __syncthreads();
+    const uint32_t ep = (uint32_t)(a.t + 1);
+    if (tid == 0) {
+      double n2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) n2 += s_dred[w];
+      const unsigned long long eph = (unsigned long long)ep << 32;
+      const unsigned long long nb = (unsigned long long)__double_as_longlong(n2);
+      st_relaxed_sys_u64(&a.range_words[r], eph | (uint32_t)mine);
+      st_relaxed_sys_u64(&a.range_words[kMaxCtas + r], eph | (nb & 0xffffffffull));
+      st_relaxed_sys_u64(&a.range_words[2 * kMaxCtas + r], eph | (nb >> 32));
+    }
+    base = cta_sum_words(a.range_words, r, ep, s_red);
+  } else {
+    base = cta_sum_counts(a.tile_count, ft, t0, s_red);
+  }
   if (r == 0) PROBE(9);
   if (r == G - 1) PROBE(10);
   CPROBE(1, r);
@@ -727,7 +803,10 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
   int64_t running = base;
   for (int cb = 0; cb < nch; cb += kThreads) {
     const int nb = nch - cb < kThreads ? nch - cb : kThreads;
-    if (cb) cnt = tid < nb ? __ldcg(&a.chunk_count[t0 * kWarps + cb + tid]) : 0;
+    // large vectors: the next batch's counts, in flight during this batch's copy
+    const int cn = cb + kThreads + tid;
+    const int cnt_next = BIG && cn < nch ? __ldcg(&a.chunk_count[t0 * kWarps + cn]) : 0;
+    if (!BIG && cb) cnt = tid < nb ? __ldcg(&a.chunk_count[t0 * kWarps + cb + tid]) : 0;
     // block exclusive scan of the chunk counts
     int incl = cnt;
 #pragma unroll
@@ -786,6 +865,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
       }
     }
     running += btot;
+    if (BIG) cnt = cnt_next;
     __syncthreads();
   }
   if (r == 0) PROBE(11);
@@ -844,8 +924,12 @@ cudaError_t launch_finish_t(const SelectArgs& a, const RunConst& rc, cudaStream_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (rc.fused) return cudaLaunchKernelEx(&cfg, finish_kernel<T, true>, a, rc);
-  return cudaLaunchKernelEx(&cfg, finish_kernel<T, false>, a, rc);
+  const bool big = a.range_words != nullptr;
+  if (rc.fused)
+    return big ? cudaLaunchKernelEx(&cfg, finish_kernel<T, true, true>, a, rc)
+               : cudaLaunchKernelEx(&cfg, finish_kernel<T, true, false>, a, rc);
+  return big ? cudaLaunchKernelEx(&cfg, finish_kernel<T, false, true>, a, rc)
+             : cudaLaunchKernelEx(&cfg, finish_kernel<T, false, false>, a, rc);
 }
 
 // ---- K4+K5: union + contributions + clear -----------------------------------
@@ -1298,7 +1382,7 @@ __device__ __noinline__ uint32_t poll_word(const unsigned long long* p, uint32_t
 constexpr int kXUnroll = 4;   // union entries per thread in flight
 constexpr int kXPeers = 4;    // peer words per entry polled together
 
-template <typename T>
+template <typename T, bool BIG>
 // 3 blocks per SM by registers: the 2-per-SM grid + block 0 is always resident
 __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, RunConst rc) {
   using P = typename Pair<T>::P;
@@ -1324,6 +1408,29 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   const uint32_t ep = (uint32_t)a.epoch;
   const Plan& plan = ctrl->plan[par];  // the epilogue writes only the other slot
 
+  if (tid == 0) {
+    // partition table from the replicated plan (allocate_partition,
+    // allocator.cpp:92-99: partition p is held by rank (p - t) mod n; the last
+    // one ends at n_g)
+    const int tm = (int)mod_floor(sa.t, n);
+    const exd_topology& tp = plan.topo;
+    int32_t tc = 0;
+    for (int p = 0; p < n; ++p) {
+      const int rk = p - tm < 0 ? p - tm + n : p - tm;
+      const int64_t pst = tp.blk_pos[p] * tp.sz_blk;
+      const int64_t pend = p == n - 1 ? rc.n_g : (tp.blk_pos[p] + tp.blk_part[p]) * tp.sz_blk;
+      s_prank[p] = rk;
+      s_ft[p] = (int32_t)(pst / TILE);
+      s_pst[p] = pst;
+      s_tcum[p] = tc;
+      tc += pend > pst ? (int32_t)((pend - 1) / TILE - pst / TILE + 1) : 0;
+    }
+    s_tcum[n] = tc;
+    // work blocks per partition, by tiles, at least one each (G >= n)
+    for (int p = 0; p <= n; ++p)
+      s_bcum[p] = p + (int32_t)(((int64_t)(G - n) * s_tcum[p]) / (tc > 0 ? tc : 1));
+  }
+  __syncthreads();  // the table is read by every block (block 0: BIG totals)
   if (r < 0) {
     // ---- block 0: totals, count exchange, control epilogue
     __shared__ EpiShared esh;
@@ -1339,7 +1446,20 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     const int nt = (int)((rc.n_g + TILE - 1) / TILE);
     double pn = 0.0;
     int64_t pk = 0;
-    for (int i = tid; i < nt; i += kSumUnroll * kThreads) {
+    if (BIG) {
+      // large vectors: own k_i from the range words of the blocks working on
+      // this rank's partition; ||e||^2 from the norm partials every work block
+      // publishes at its end (fixed order: thread i takes blocks i, i + 256, ...)
+      const int po = (int)mod_floor(sa.t + me, n);  // allocate_partition: (t % n + rank) % n
+      for (int q = s_bcum[po] + tid; q < s_bcum[po + 1]; q += kThreads)
+        pk += poll_word(&a.xrange_words[q], ep, a.err);
+      for (int q = tid; q < G; q += kThreads) {
+        const unsigned long long lo = poll_word(&a.xrange_words[kMaxCtas + q], ep, a.err);
+        const unsigned long long hi = poll_word(&a.xrange_words[2 * kMaxCtas + q], ep, a.err);
+        pn += __longlong_as_double((long long)((hi << 32) | lo));
+      }
+    }
+    for (int i = tid; i < (BIG ? 0 : nt); i += kSumUnroll * kThreads) {
       double v[kSumUnroll];
       int c[kSumUnroll];
 #pragma unroll
@@ -1404,28 +1524,6 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   }
 
   // ---- work blocks
-  if (tid == 0) {
-    // partition table from the replicated plan (allocate_partition,
-    // allocator.cpp:92-99: partition p is held by rank (p - t) mod n; the last
-    // one ends at n_g)
-    const int tm = (int)mod_floor(sa.t, n);
-    const exd_topology& tp = plan.topo;
-    int32_t tc = 0;
-    for (int p = 0; p < n; ++p) {
-      const int rk = p - tm < 0 ? p - tm + n : p - tm;
-      const int64_t pst = tp.blk_pos[p] * tp.sz_blk;
-      const int64_t pend = p == n - 1 ? rc.n_g : (tp.blk_pos[p] + tp.blk_part[p]) * tp.sz_blk;
-      s_prank[p] = rk;
-      s_ft[p] = (int32_t)(pst / TILE);
-      s_pst[p] = pst;
-      s_tcum[p] = tc;
-      tc += pend > pst ? (int32_t)((pend - 1) / TILE - pst / TILE + 1) : 0;
-    }
-    s_tcum[n] = tc;
-    // work blocks per partition, by tiles, at least one each (G >= n)
-    for (int p = 0; p <= n; ++p)
-      s_bcum[p] = p + (int32_t)(((int64_t)(G - n) * s_tcum[p]) / (tc > 0 ? tc : 1));
-  }
   // No griddepcontrol.wait yet: the partition's runs and counts arrive as words
   // (this rank's own too), so the lookups below overlap this rank's stream
   // kernel draining its remote stores. The wait comes before the first access
@@ -1458,7 +1556,47 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     // base: the counts of every tile before t0 in partition order (tiles of
     // partitions < p, then [ftp, t0) of p), as words
     int64_t base = 0, poff = 0;  // union position of t0's first entry / of partition p
-    {
+    if (BIG) {
+      // large vectors: this block's range count from the holder's tile words,
+      // published as a word; base / poff from the earlier blocks' words (the
+      // blocks run in partition order, then tile order)
+      int64_t mine = 0;
+      const unsigned long long* tw = a.tile_in[par][rk];
+      for (int f = t0 + tid; f < t1; f += kThreads) {
+        const unsigned long long w = ld_relaxed_sys_u64(&tw[f]);
+        mine += (uint32_t)(w >> 32) == ep ? (uint32_t)w : poll_word(&tw[f], ep, a.err);
+      }
+      mine = warp_sum(mine);
+      if (lane == 0) s_red[warp] = mine;
+      __syncthreads();
+      if (tid == 0) {
+        int64_t m = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) m += s_red[w];
+        st_relaxed_sys_u64(&a.xrange_words[r], ((unsigned long long)ep << 32) | (uint32_t)m);
+      }
+      int64_t sb = 0, sp_ = 0;
+      for (int q = tid; q < r; q += kThreads) {
+        const uint32_t c = poll_word(&a.xrange_words[q], ep, a.err);
+        sb += c;
+        if (q < s_bcum[p]) sp_ += c;
+      }
+      sb = warp_sum(sb);
+      sp_ = warp_sum(sp_);
+      __shared__ int64_t s_redb[kWarps];
+      __syncthreads();
+      if (lane == 0) {
+        s_red[warp] = sb;
+        s_redb[warp] = sp_;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        base += s_red[w];
+        poff += s_redb[w];
+      }
+      __syncthreads();
+    } else {
       const int F = s_tcum[p] + (t0 - ftp), Fp = s_tcum[p];
       int64_t sum = 0, sum_before = 0;
       for (int f0 = tid; f0 < F; f0 += kSumUnroll * kThreads) {
@@ -1674,6 +1812,27 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       }
       running += btot;
       __syncthreads();
+    }
+  }
+  if (BIG) {
+    // the ||e||^2 partial of an equal slice of all tiles, for block 0's totals
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // returns at once if passed
+    const int nt = (int)((rc.n_g + TILE - 1) / TILE);
+    const int n0 = (int)(((int64_t)nt * r) / G), n1 = (int)(((int64_t)nt * (r + 1)) / G);
+    double pn = 0.0;
+    for (int i = n0 + tid; i < n1; i += kThreads) pn += __ldcg(&sa.tile_norm[i]);
+    pn = warp_sum(pn);
+    __syncthreads();
+    if (lane == 0) s_dred[warp] = pn;
+    __syncthreads();
+    if (tid == 0) {
+      double n2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) n2 += s_dred[w];
+      const unsigned long long eph = (unsigned long long)ep << 32;
+      const unsigned long long nb = (unsigned long long)__double_as_longlong(n2);
+      st_relaxed_sys_u64(&a.xrange_words[kMaxCtas + r], eph | (nb & 0xffffffffull));
+      st_relaxed_sys_u64(&a.xrange_words[2 * kMaxCtas + r], eph | (nb >> 32));
     }
   }
   if (r == 0) PROBE(9);
@@ -2264,8 +2423,12 @@ cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s) 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (rc.dtype == EXD_F64) return cudaLaunchKernelEx(&cfg, exchange_kernel<double>, a, rc);
-  return cudaLaunchKernelEx(&cfg, exchange_kernel<float>, a, rc);
+  const bool big = a.xrange_words != nullptr;
+  if (rc.dtype == EXD_F64)
+    return big ? cudaLaunchKernelEx(&cfg, exchange_kernel<double, true>, a, rc)
+               : cudaLaunchKernelEx(&cfg, exchange_kernel<double, false>, a, rc);
+  return big ? cudaLaunchKernelEx(&cfg, exchange_kernel<float, true>, a, rc)
+             : cudaLaunchKernelEx(&cfg, exchange_kernel<float, false>, a, rc);
 }
 
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {

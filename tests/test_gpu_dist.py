@@ -86,3 +86,12 @@ def test_dead_peer_fails_the_step_instead_of_hanging(sync):
     # path: the kernels' 20 s poll limit. Then the engine refuses further steps.
     _run(2, "--sync", sync, "--kill-peer", "1", port=29588 if sync == "nccl" else 29589,
          env={"EXD_NCCL_TIMEOUT_S": "5"})
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["p2p", "p2p-pull"])
+def test_two_ranks_large_vector_published_range_counts(sync):
+    # n_g > 3072 tiles: the exchange / finish kernels take their bases from the
+    # blocks' published range words instead of summing every earlier tile
+    _run(2, "--sync", sync, "--n_g", "20000003", "--steps", "6", "--skew", "0",
+         port=29590 if sync == "p2p" else 29591)
