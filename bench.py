@@ -321,6 +321,17 @@ def cpu_baseline(wl, grad_fn, budget_s):
                         "density_mean": statistics.mean(r.density for r in recs[warm:])}
         except Exception as e:
             out[key] = {"unavailable": str(e)}
+    if wl.default and wl.n == 1:
+        # configs[0]: the same gradient size with 2 simulated workers, the reference's own
+        # CPU run (BASELINE.json configs[0]); the reference runs one thread per worker
+        try:
+            wl2 = Workload(2, n_g=wl.n_g, d=wl.d)
+            ms, times, recs = cpu_run("reference", wl2, reference_grad_fn(wl2), steps=20,
+                                      warmup=warm, budget_s=budget_s)
+            out["configs0_n2_as_shipped"] = {"median_ms": ms, "mean_ms": statistics.mean(times),
+                                             "steps": len(times), "warmup": warm, "cores": 2}
+        except Exception as e:
+            out["configs0_n2_as_shipped"] = {"unavailable": str(e)}
     v = out.get("as_shipped", {}).get("median_ms")
     return {"value": v, "unit": UNIT, "cores": wl.n, "kind": "reference",
             "sample": f"median over up to 50 Engine::step() calls (fewer when a step would "

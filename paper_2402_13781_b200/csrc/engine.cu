@@ -252,6 +252,8 @@ struct exd_engine {
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
   unsigned long long* xrange_words = nullptr;  // push-reduce, large vectors: [3][kMaxCtas]
+  int two_pass = -1;                  // exchange work loop: -1 by size, 0/1 forced (EXD_TWO_PASS)
+  int xchg_blocks = 444;              // exchange work blocks (3 per SM - 1)
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
   //   | chunk counts[2][n] | tile counts[2][n] | contrib[2][n][n_g]   ([2]: step parity;
@@ -747,6 +749,12 @@ int setup_p2p(exd_engine* h) {
   *h->p2p_err = 0;
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
   if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
+  if (const char* tp = std::getenv("EXD_TWO_PASS")) h->two_pass = tp[0] == '1' ? 1 : 0;
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->xchg_blocks = 3 * sms - 1;
+  }
   if (h->xchg && h->tiles > kBaseRoundTiles)
     if (int r2 = alloc_zero((void**)&h->xrange_words, sizeof(unsigned long long) * 3 * kMaxCtas))
       return r2;
@@ -858,6 +866,9 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   o.err = h->p2p_err_dev;
   o.me = wk.rank;
   o.xrange_words = h->xrange_words;
+  // more than one iteration of the one-pass loop per work block expected
+  // (k entries over ~3 blocks per SM, 4 per thread in flight): two passes
+  o.two_pass = h->two_pass >= 0 ? h->two_pass : (h->cfg.k > (int64_t)h->xchg_blocks * 4 * 256 ? 1 : 0);
   return o;
 }
 

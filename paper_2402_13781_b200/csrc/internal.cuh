@@ -210,6 +210,7 @@ struct ExchangeArgs {
   unsigned long long epoch;          // t + 1
   unsigned int* err;                 // set on a peer timeout (device memory)
   int32_t me;
+  int32_t two_pass;                  // large k': the work loop in two passes (exchange_kernel)
   unsigned long long* xrange_words;  // large vectors: [3][kMaxCtas] work blocks' range counts
                                      // and ||e||^2 halves as {payload, epoch} words
                                      // (nullptr: small vector)

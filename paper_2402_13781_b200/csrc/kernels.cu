@@ -1379,10 +1379,39 @@ __device__ __noinline__ uint32_t poll_word(const unsigned long long* p, uint32_t
   return (uint32_t)w;
 }
 
+// Poll one {value, epoch} contribution / sum until it carries `ep`; gives up
+// after 20 s (sets *err) so a dead peer cannot hang the GPU.
+template <typename T>
+__device__ __forceinline__ T poll_ll(const unsigned long long* w, uint32_t ep, unsigned int* err) {
+  T v;
+  if (LL<T>::get(w, ep, v)) return v;
+  const unsigned long long t0 = gtime_ns();
+  unsigned spins = 0;
+  while (!LL<T>::get(w, ep, v)) {
+    if ((++spins & 255u) == 0 &&
+        (gtime_ns() - t0 > 20000000000ull || *(volatile unsigned int*)err)) {
+      atomicExch(err, 1u);
+      break;
+    }
+    __nanosleep(20);
+  }
+  return v;
+}
+
 constexpr int kXUnroll = 4;   // union entries per thread in flight
+constexpr int kX2Unroll = 4;  // pass-2 positions per thread in flight (TWO)
 constexpr int kXPeers = 4;    // peer words per entry polled together
 
-template <typename T, bool BIG>
+// TWO (large k'): the work loop runs in two passes per block, so no NVLink
+// round trip sits inside an iteration. Pass 1 streams the block's entries:
+// index words, own contribution (also into this rank's own inbox slot), the
+// contributions out, union entry, residual clear. Pass 2 streams the block's
+// contiguous union positions: the n contribution words (they were posted
+// during the peers' pass 1, so the polls rarely wait) or the holder's sum,
+// the rank-order sum and x -= g/n. Small k' keeps the one-pass loop, which
+// needs one iteration per block and overlaps the lookups with the stream
+// kernel's drain.
+template <typename T, bool BIG, bool TWO>
 // 3 blocks per SM by registers: the 2-per-SM grid + block 0 is always resident
 __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, RunConst rc) {
   using P = typename Pair<T>::P;
@@ -1698,9 +1727,11 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         // x is not written by the stream kernel (the previous step's kernels
         // completed before it started): gather it before the wait
         T xv[kXUnroll];
+        if (!TWO) {
 #pragma unroll
-        for (int q = 0; q < kXUnroll; ++q)
-          if (i0 + q * kThreads < btot) xv[q] = x[jj[q]];
+          for (int q = 0; q < kXUnroll; ++q)
+            if (i0 + q * kThreads < btot) xv[q] = x[jj[q]];
+        }
         // from here on: what this rank's stream kernel wrote (e, staged values)
         asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef EXD_PROBE
@@ -1723,6 +1754,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
           } else if (!own) {  // to the partition's holder, which sums and sends the sum back
             LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rk]) + pos * W, vv[q], ep);
           }
+          if (TWO && (!hs || own))  // pass 2 sums every source's word, own included
+            LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][me]) + pos * W, vv[q], ep);
           a.idx_global[pos] = jj[q];
           if (own) {  // this rank's ascending selection (partition-local index)
             sa.idx[pos - poff] = jj[q];
@@ -1734,6 +1767,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
 #ifdef EXD_PROBE
         PROBE_MAX(43);
 #endif
+        if (TWO) continue;  // pass 2 below
         // the peers' contributions for the same positions; rank-order sum (the
         // holder only, under the holder sum; the others poll the holder's sum)
         T sv[kXUnroll];
@@ -1812,6 +1846,43 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       }
       running += btot;
       __syncthreads();
+    }
+    if (TWO) {
+      // pass 2 over this block's union positions [base, running)
+      const bool sums = !hs || own;  // this rank sums the n words (else: the holder's sum)
+      for (int64_t p0 = base + tid; p0 < running; p0 += kX2Unroll * kThreads) {
+        int32_t jj[kX2Unroll];
+        T xv[kX2Unroll], sv[kX2Unroll];
+#pragma unroll
+        for (int q = 0; q < kX2Unroll; ++q) {
+          const int64_t pos = p0 + (int64_t)q * kThreads;
+          if (pos < running) jj[q] = a.idx_global[pos];
+        }
+#pragma unroll
+        for (int q = 0; q < kX2Unroll; ++q)
+          if (p0 + (int64_t)q * kThreads < running) xv[q] = x[jj[q]];
+#pragma unroll
+        for (int q = 0; q < kX2Unroll; ++q) {
+          const int64_t pos = p0 + (int64_t)q * kThreads;
+          if (pos >= running) continue;
+          if (sums) {  // rank order, as all_reduce_sum (collectives.cpp:62-68)
+            for (int rr = 0; rr < n; ++rr) {
+              const T v = poll_ll<T>(static_cast<const unsigned long long*>(a.contrib_in[par][rr]) +
+                                         pos * W, ep, a.err);
+              sv[q] = rr == 0 ? v : sv[q] + v;
+            }
+            if (hs)  // the holder sends the sum to every peer
+              for (int rr = 0; rr < n; ++rr)
+                if (rr != me)
+                  LL<T>::put(static_cast<unsigned long long*>(a.sum_out[par][rr]) + pos * W, sv[q], ep);
+          } else {
+            sv[q] = poll_ll<T>(static_cast<const unsigned long long*>(a.sum_in[par]) + pos * W, ep,
+                               a.err);
+          }
+          gsum[pos] = sv[q];
+          x[jj[q]] = apply_update<T>(xv[q], sv[q], n);
+        }
+      }
     }
   }
   if (BIG) {
@@ -2424,11 +2495,14 @@ cudaError_t launch_exchange(const ExchangeArgs& a, RunConst rc, cudaStream_t s) 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool big = a.xrange_words != nullptr;
+  const bool two = a.two_pass != 0;
+#define EXD_XK(T_, B_, P_) cudaLaunchKernelEx(&cfg, exchange_kernel<T_, B_, P_>, a, rc)
   if (rc.dtype == EXD_F64)
-    return big ? cudaLaunchKernelEx(&cfg, exchange_kernel<double, true>, a, rc)
-               : cudaLaunchKernelEx(&cfg, exchange_kernel<double, false>, a, rc);
-  return big ? cudaLaunchKernelEx(&cfg, exchange_kernel<float, true>, a, rc)
-             : cudaLaunchKernelEx(&cfg, exchange_kernel<float, false>, a, rc);
+    return big ? (two ? EXD_XK(double, true, true) : EXD_XK(double, true, false))
+               : (two ? EXD_XK(double, false, true) : EXD_XK(double, false, false));
+  return big ? (two ? EXD_XK(float, true, true) : EXD_XK(float, true, false))
+             : (two ? EXD_XK(float, false, true) : EXD_XK(float, false, false));
+#undef EXD_XK
 }
 
 cudaError_t launch_cap(const CapArgs& a, RunConst rc, cudaStream_t s) {

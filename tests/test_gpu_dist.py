@@ -95,3 +95,20 @@ def test_two_ranks_large_vector_published_range_counts(sync):
     # blocks' published range words instead of summing every earlier tile
     _run(2, "--sync", sync, "--n_g", "20000003", "--steps", "6", "--skew", "0",
          port=29590 if sync == "p2p" else 29591)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("holder_sum", ["0", "1"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_two_ranks_two_pass_exchange(holder_sum, dtype):
+    # the two-pass exchange loop (chosen by size at large k'), forced on
+    _run(2, "--sync", "p2p", "--dtype", dtype, "--steps", "10", "--density", "0.05",
+         port=29592 + 2 * (dtype == "f64") + int(holder_sum),
+         env={"EXD_TWO_PASS": "1", "EXD_HOLDER_SUM": holder_sum})
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_two_pass_exchange_holder_sum():
+    _run(4, "--sync", "p2p", "--steps", "10", "--density", "0.05", port=29596,
+         env={"EXD_TWO_PASS": "1"})
+    _run(4, "--sync", "p2p", "--n_g", "20000003", "--steps", "5", "--skew", "0", port=29597)

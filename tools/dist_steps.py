@@ -20,18 +20,28 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--sync", default="auto")
     a = ap.parse_args()
+    import time
     import torch
-    import torch.distributed as dist
     from paper_2402_13781_b200 import sparsim as S
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("gloo")
-    ids = [S.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(ids, src=0)
+    # the NCCL id through a file, not gloo: a rank started under a profiler can
+    # take long enough to start that gloo's connect retries run out
+    path = f"/tmp/exd_ncclid_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        nid = S.nccl_unique_id()
+        with open(path + ".tmp", "wb") as f:
+            f.write(nid)
+        os.replace(path + ".tmp", path)
+    else:
+        t0 = time.time()  # a file left by an earlier run is older than this process
+        while not (os.path.exists(path) and os.path.getmtime(path) > t0 - 30):
+            time.sleep(0.05)
+        nid = open(path, "rb").read()
     cfg = S.SparsifierConfig(n=world, n_g=a.n_g, n_b=256, d=a.density, seed=7)
     eng = S.Engine.rank(cfg, S.EngineOptions(verify_replication=False, sync=a.sync), rank, local,
-                        ids[0])
+                        nid)
     src = S.SyntheticStream(S.StreamSpec(n_g=a.n_g, seed=7))
     bufs = [torch.empty(a.n_g, device=f"cuda:{local}") for _ in range(2)]
     for t in range(a.warmup + a.steps):
@@ -43,9 +53,9 @@ def main():
     if rank == 0:
         print(f"dist_steps world={world} n_g={a.n_g} d={a.density} sync={eng.sync_mode()} "
               f"t={rec.t} k'={rec.k_prime} k_rank={rec.k_rank}", flush=True)
-    dist.barrier()
-    eng.close()
-    dist.destroy_process_group()
+    eng.close()  # the teardown barrier is collective (NCCL)
+    if rank == 0:
+        os.remove(path)
 
 
 if __name__ == "__main__":
