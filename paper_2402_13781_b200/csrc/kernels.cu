@@ -509,16 +509,24 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
             const uint32_t j = lbeg + u * 32 * VN + c;
             // the finish kernel reads the pair right after the stream: keep
             // it in L2 past the streaming data
+#ifdef EXD_XP_PLAIN_PAIR
+            sp[pos] = Pair<T>::make(j, v[u][c]);
+#else
             Pair<T>::store_keep(&sp[pos], Pair<T>::make(j, v[u][c]), keep);
+#endif
             if (PUSH) s_run[warp * CH + (pos - sbase)] = (int32_t)j;
+#ifndef EXD_XP_NO_BLK
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
+#endif
             ++pos;
           }
         }
       }
       running += (int)(__popc(b0) + 2u * __popc(b1) + 4u * __popc(b2));
     }
+#ifndef EXD_XP_NO_BLK
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
+#endif
     if (PUSH && running) {
       // the run sbase + [0, running) in every peer's staging slot as
       // {index, epoch} words: 256 B coalesced stores, each word its own flag

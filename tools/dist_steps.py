@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--sync", default="auto")
+    ap.add_argument("--leak", action="store_true",
+                    help="exit without the collective teardown (a profiled rank may lag)")
     a = ap.parse_args()
     import time
     import torch
@@ -53,9 +55,12 @@ def main():
     if rank == 0:
         print(f"dist_steps world={world} n_g={a.n_g} d={a.density} sync={eng.sync_mode()} "
               f"t={rec.t} k'={rec.k_prime} k_rank={rec.k_rank}", flush=True)
-    eng.close()  # the teardown barrier is collective (NCCL)
-    if rank == 0:
+    if rank == 0 and os.path.exists(path):
         os.remove(path)
+    if a.leak:
+        eng.h = None  # the driver reclaims everything at exit
+        return
+    eng.close()  # the teardown barrier is collective (NCCL)
 
 
 if __name__ == "__main__":

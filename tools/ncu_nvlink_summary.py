@@ -29,9 +29,10 @@ def parse(path):
 
 def main():
     dst, files = sys.argv[1], sys.argv[2:]
-    res = {"source": "ncu --metrics nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,"
-                     "gpu__time_duration.sum --clock-control none --cache-control none "
-                     "(tools/nvlink_ncu.sh; one ncu per rank, single pass, serialised launches)",
+    res = {"source": "ncu --metrics nvltx__bytes.sum,gpu__time_duration.sum --clock-control none "
+                     "--cache-control none (tools/nvlink_ncu.sh; every rank under its own ncu, "
+                     "one counter so a single pass, serialised launches); nvltx counts link "
+                     "bytes at 32 B granularity, protocol included",
            "peak_gbs_measured": 770.0, "peak_gbs_nominal": 900.0, "captures": []}
     for f in files:
         m = re.search(r"nvl_n(\d+)_(\d+)_([0-9.]+)_rank(\d+)\.csv", f)
@@ -40,19 +41,17 @@ def main():
         n, ng, d, rank = int(m[1]), int(m[2]), float(m[3]), int(m[4])
         for kind, ls in parse(f).items():
             tx = statistics.mean(l.get("nvltx__bytes.sum", 0.0) for l in ls)
-            rx = statistics.mean(l.get("nvlrx__bytes.sum", 0.0) for l in ls)
-            user = statistics.mean(l.get("nvltx__bytes_data_user.sum", 0.0) for l in ls)
             dur = statistics.mean(l.get("gpu__time_duration.sum", 0.0) for l in ls) * 1e-9
             res["captures"].append({
                 "n": n, "n_g": ng, "d": d, "rank": rank, "kernel": kind, "launches": len(ls),
-                "nvltx_bytes": tx, "nvlrx_bytes": rx, "nvltx_user_bytes": user,
+                "nvltx_bytes": tx,
                 "duration_us": dur * 1e6,
                 "tx_gbs": tx / dur / 1e9 if dur else None,
                 "tx_frac_of_measured": tx / dur / 770e9 if dur else None})
     json.dump(res, open(dst, "w"), indent=1)
     for c in res["captures"]:
         print(f"n={c['n']} n_g={c['n_g']} d={c['d']} rank {c['rank']} {c['kernel']:16s} "
-              f"tx {c['nvltx_bytes'] / 1e6:9.3f} MB rx {c['nvlrx_bytes'] / 1e6:9.3f} MB "
+              f"tx {c['nvltx_bytes'] / 1e6:9.3f} MB "
               f"{c['duration_us']:9.1f} us -> {c['tx_gbs'] or 0:7.1f} GB/s "
               f"({(c['tx_frac_of_measured'] or 0) * 100:.1f}% of 770)")
 
