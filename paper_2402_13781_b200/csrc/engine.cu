@@ -252,6 +252,10 @@ struct exd_engine {
   unsigned int* p2p_err_dev = nullptr;  // device word: peer timeout
   unsigned long long* p2p_gate = nullptr;  // [3] local gate words + arrive counter
   unsigned long long* xrange_words = nullptr;  // push-reduce, large vectors: [3][kMaxCtas]
+  int64_t xcap = 0;                   // push-reduce contribution capacity (union positions)
+  std::vector<void*> spill_peer[2];   // [n] every rank's exported spill buffer (own: local)
+  std::vector<unsigned long long*> spill_flag_out[2];  // [n] my flag row in every inbox
+  unsigned long long* spill_flag_in[2] = {nullptr, nullptr};  // own flag area [n][kMaxCtas]
   int two_pass = -1;                  // exchange work loop: -1 by size, 0/1 forced (EXD_TWO_PASS)
   int xchg_blocks = 444;              // exchange work blocks (3 per SM - 1)
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
@@ -611,7 +615,16 @@ int setup_p2p(exd_engine* h) {
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   size_t flags_b = 0, list_b = 0, con_b = 0, off_lists = 0, off_c0 = 0, off_c1 = 0, total = 0;
   size_t stage_b = 0, chunk_b = 0, tile_b = 0, xcon_b = 0, off_st = 0, off_ch = 0, off_ti = 0, off_xc = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  // push-reduce contribution capacity in union positions: n_g (every position
+  // a word slot per source) unless that does not fit or EXD_PUSH_CAP says
+  // otherwise; positions past it spill to a pull from the sources' exported
+  // buffers (exchange kernel). Halved per failed attempt down to a floor.
+  const int64_t k_floor = std::max<int64_t>(1 << 20, 2 * h->cfg.k);
+  int64_t xcap = h->cfg.n_g;
+  if (const char* pc = std::getenv("EXD_PUSH_CAP")) xcap = std::max<int64_t>(1, std::atoll(pc));
+  xcap = std::min<int64_t>(xcap, h->cfg.n_g);
+  size_t spill_b = 0, sflag_b = 0, off_sp = 0, off_sf = 0;
+  for (int attempt = 0; attempt < 64; ++attempt) {
     if (h->xchg) {
       // push-reduce: flags[2][n] | stage[2] | chunk counts[2][n] | tile counts[2][n]
       //              | contributions[2][n]; words: 8 B per index / count / fp32 value, 16 B per fp64.
@@ -621,12 +634,17 @@ int setup_p2p(exd_engine* h) {
       stage_b = al(8 * ((size_t)h->cfg.n_g + 2 * (size_t)h->tile));
       chunk_b = al(8 * (size_t)(h->tiles + 1) * kChunksPerTile);
       tile_b = al(8 * (size_t)(h->tiles + 8));
-      xcon_b = al(2 * h->esz * (size_t)h->cfg.n_g);
+      xcon_b = al(2 * h->esz * (size_t)xcap);
+      const bool spill = xcap < h->cfg.n_g;
+      spill_b = spill ? al(h->esz * (size_t)h->cfg.n_g) : 0;  // [2] own contributions to pull
+      sflag_b = spill ? al(8 * (size_t)n * kMaxCtas) : 0;     // [2][source][work block]
       off_st = flags_b;
       off_ch = off_st + stage_b * 2;
       off_ti = off_ch + chunk_b * 2 * n;
       off_xc = off_ti + tile_b * 2 * n;
-      total = off_xc + xcon_b * 2 * n + xcon_b * 2;  // + the holder-sum slots [2]
+      off_sp = off_xc + xcon_b * 2 * n + xcon_b * 2;  // after the holder-sum slots [2]
+      off_sf = off_sp + spill_b * 2;
+      total = off_sf + sflag_b * 2;
     } else {
       // pull-reduce: flags[n] | lists[n][cap_part] | contrib[2][n_g]
       flags_b = al(sizeof(PeerFlags) * (size_t)n);
@@ -654,8 +672,13 @@ int setup_p2p(exd_engine* h) {
     if (h->region) cudaFree(h->region);
     h->region = nullptr;
     if (!h->xchg) return set_err(EXD_ECUDA, "peer-memory inbox does not fit in device memory");
-    h->xchg = false;  // the push-reduce inbox does not fit (huge n_g): pull-reduce
+    if (xcap > k_floor) {  // a smaller contribution capacity, spilling past it
+      xcap = std::max<int64_t>(k_floor, xcap / 2);
+      continue;
+    }
+    h->xchg = false;  // even the floor does not fit: pull-reduce
   }
+  h->xcap = h->xchg ? xcap : 0;
   CU(cudaMemset(h->region, 0, flags_b));
   // words start with epoch 0 (never a live epoch)
   if (h->xchg) CU(cudaMemset(static_cast<char*>(h->region) + off_st, 0, total - off_st));
@@ -718,6 +741,19 @@ int setup_p2p(exd_engine* h) {
       }
     }
     for (int r = 0; r < n; ++r) h->slot_host[r] = reinterpret_cast<PeerFlags*>(base[r]) + me;
+    if (h->xcap < h->cfg.n_g) {
+      for (int par = 0; par < 2; ++par) {
+        h->spill_peer[par].assign(n, nullptr);
+        h->spill_flag_out[par].assign(n, nullptr);
+        for (int r = 0; r < n; ++r) {
+          h->spill_peer[par][r] = base[r] + off_sp + spill_b * par;
+          // my row of r's flag area [par][source = me][work block]
+          h->spill_flag_out[par][r] = reinterpret_cast<unsigned long long*>(
+              base[r] + off_sf + sflag_b * par) + (size_t)me * kMaxCtas;
+        }
+        h->spill_flag_in[par] = reinterpret_cast<unsigned long long*>(own + off_sf + sflag_b * par);
+      }
+    }
     // every rank must agree: the choice depends only on n (and the same
     // environment on every rank)
     h->holder_sum = n >= 4;
@@ -869,6 +905,17 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   // more than one iteration of the one-pass loop per work block expected
   // (k entries over ~3 blocks per SM, 4 per thread in flight): two passes
   o.two_pass = h->two_pass >= 0 ? h->two_pass : (h->cfg.k > (int64_t)h->xchg_blocks * 4 * 256 ? 1 : 0);
+  o.xcap = h->xcap;
+  if (h->xcap < h->cfg.n_g) {
+    o.two_pass = 1;  // the spill pull lives in pass 2
+    for (int par = 0; par < 2; ++par) {
+      for (int r = 0; r < h->n; ++r) {
+        o.spill_peer[par][r] = h->spill_peer[par][r];
+        o.spill_flag_out[par][r] = h->spill_flag_out[par][r];
+      }
+      o.spill_flag_in[par] = h->spill_flag_in[par];
+    }
+  }
   return o;
 }
 

@@ -211,6 +211,13 @@ struct ExchangeArgs {
   unsigned int* err;                 // set on a peer timeout (device memory)
   int32_t me;
   int32_t two_pass;                  // large k': the work loop in two passes (exchange_kernel)
+  // bounded contribution slots: union positions >= xcap are not pushed; each
+  // source writes them to its exported spill buffer, raises a per-block flag
+  // in every peer's inbox, and the peers pull them (pass 2)
+  int64_t xcap;
+  void* spill_peer[2][EXD_MAX_WORKERS];                 // [parity][source] spill buffers
+  unsigned long long* spill_flag_out[2][EXD_MAX_WORKERS];  // [parity][dest] my flag row
+  unsigned long long* spill_flag_in[2];                  // [parity] own flags [source][block]
   unsigned long long* xrange_words;  // large vectors: [3][kMaxCtas] work blocks' range counts
                                      // and ||e||^2 halves as {payload, epoch} words
                                      // (nullptr: small vector)

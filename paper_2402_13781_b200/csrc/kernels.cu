@@ -351,8 +351,9 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
   static_assert(CH * kWarps == tile_of<T>(), "tile = kWarps chunks");
   __shared__ double s_norm[kWarps];
   __shared__ int s_cnt[kWarps];
-  // PUSH: each warp's run of staged indices, copied to the peers coalesced
-  __shared__ int32_t s_run[PUSH ? kWarps * CH : 1];
+  // each warp's run of (index, value) pairs, compacted here and then written
+  // to the staging buffer (and, PUSH, to the peers) with coalesced stores
+  __shared__ typename Pair<T>::P s_pair[SELECT ? kWarps * CH : 1];
 
   const Ctrl* ctrl = a.ctrl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     else
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(keep));
     typename Pair<T>::P* sp = static_cast<typename Pair<T>::P*>(a.stage);
+    typename Pair<T>::P* spw = s_pair + warp * CH;  // this warp's run, compacted
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t nib = (flags >> (u * VN)) & ((1u << VN) - 1u);
@@ -502,19 +504,15 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
       const uint32_t b1 = __ballot_sync(0xffffffffu, cnt & 2u);
       const uint32_t b2 = __ballot_sync(0xffffffffu, cnt & 4u);
       if (nib) {
-        uint32_t pos = sbase + running + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+        uint32_t pos = running + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
             const uint32_t j = lbeg + u * 32 * VN + c;
-            // the finish kernel reads the pair right after the stream: keep
-            // it in L2 past the streaming data
-#ifdef EXD_XP_PLAIN_PAIR
-            sp[pos] = Pair<T>::make(j, v[u][c]);
-#else
-            Pair<T>::store_keep(&sp[pos], Pair<T>::make(j, v[u][c]), keep);
+#ifdef EXD_XP_DIRECT_PAIR
+            Pair<T>::store_keep(&sp[sbase + pos], Pair<T>::make(j, v[u][c]), keep);
 #endif
-            if (PUSH) s_run[warp * CH + (pos - sbase)] = (int32_t)j;
+            spw[pos] = Pair<T>::make(j, v[u][c]);
 #ifndef EXD_XP_NO_BLK
             if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
 #endif
@@ -527,15 +525,23 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
 #ifndef EXD_XP_NO_BLK
     if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
 #endif
-    if (PUSH && running) {
-      // the run sbase + [0, running) in every peer's staging slot as
-      // {index, epoch} words: 256 B coalesced stores, each word its own flag
+    if (running) {
       __syncwarp();
-      const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
-      for (int q = 0; q < a.k1_npush; ++q) {
-        unsigned long long* dst = a.push_stage[q] + sbase;
-        for (int i = lane; i < running; i += 32)
-          st_relaxed_sys_u64(dst + i, eph | (uint32_t)s_run[warp * CH + i]);
+#ifndef EXD_XP_DIRECT_PAIR
+      // the run sbase + [0, running) with coalesced stores: a warp instruction
+      // writes 32 consecutive pairs (the finish / exchange kernels read them
+      // right after the stream: kept in L2 past the streaming data when small)
+      for (int i = lane; i < running; i += 32) Pair<T>::store_keep(&sp[sbase + i], spw[i], keep);
+#endif
+      if (PUSH) {
+        // and in every peer's staging slot as {index, epoch} words: 256 B
+        // coalesced stores, each word its own flag
+        const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
+        for (int q = 0; q < a.k1_npush; ++q) {
+          unsigned long long* dst = a.push_stage[q] + sbase;
+          for (int i = lane; i < running; i += 32)
+            st_relaxed_sys_u64(dst + i, eph | Pair<T>::idx(spw[i]));
+        }
       }
     }
   }
@@ -1387,6 +1393,19 @@ __device__ __noinline__ uint32_t poll_word(const unsigned long long* p, uint32_t
   return (uint32_t)w;
 }
 
+// relaxed system-scope load of one value (peer memory, after an acquire fence)
+template <typename T> __device__ __forceinline__ T ld_relaxed_sys_t(const T* p);
+template <> __device__ __forceinline__ float ld_relaxed_sys_t<float>(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+template <> __device__ __forceinline__ double ld_relaxed_sys_t<double>(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Poll one {value, epoch} contribution / sum until it carries `ep`; gives up
 // after 20 s (sets *err) so a dead peer cannot hang the GPU.
 template <typename T>
@@ -1755,14 +1774,17 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
           const int i = i0 + q * kThreads;
           if (i >= btot) continue;
           const int64_t pos = running + i;
-          if (!hs) {  // to every peer: each rank sums all n itself
+          if (TWO && pos >= a.xcap) {
+            // past the contribution slots: the peers pull it (pass 2)
+            static_cast<T*>(a.spill_peer[par][me])[pos] = vv[q];
+          } else if (!hs) {  // to every peer: each rank sums all n itself
             for (int rr = 0; rr < n; ++rr)
               if (rr != me)
                 LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rr]) + pos * W, vv[q], ep);
           } else if (!own) {  // to the partition's holder, which sums and sends the sum back
             LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][rk]) + pos * W, vv[q], ep);
           }
-          if (TWO && (!hs || own))  // pass 2 sums every source's word, own included
+          if (TWO && pos < a.xcap && (!hs || own))  // pass 2 sums every source's word, own included
             LL<T>::put(static_cast<unsigned long long*>(a.contrib_out[par][me]) + pos * W, vv[q], ep);
           a.idx_global[pos] = jj[q];
           if (own) {  // this rank's ascending selection (partition-local index)
@@ -1856,6 +1878,22 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       __syncthreads();
     }
     if (TWO) {
+      // spilled positions (past the contribution slots): publish this block's
+      // spill writes to the peers, then wait for theirs (one flag per source
+      // and block; every rank splits the union the same way)
+      const bool spills = running > a.xcap;
+      if (spills) {
+        __syncthreads();  // the block's spill stores, before the fence
+        if (tid == 0) {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          for (int rr = 0; rr < n; ++rr)
+            if (rr != me) st_relaxed_sys_u64(a.spill_flag_out[par][rr] + r, ep);
+          for (int rr = 0; rr < n; ++rr)
+            if (rr != me) poll_word(a.spill_flag_in[par] + (size_t)rr * kMaxCtas + r, ep, a.err);
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+        }
+        __syncthreads();
+      }
       // pass 2 over this block's union positions [base, running)
       const bool sums = !hs || own;  // this rank sums the n words (else: the holder's sum)
       for (int64_t p0 = base + tid; p0 < running; p0 += kX2Unroll * kThreads) {
@@ -1873,7 +1911,12 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         for (int q = 0; q < kX2Unroll; ++q) {
           const int64_t pos = p0 + (int64_t)q * kThreads;
           if (pos >= running) continue;
-          if (sums) {  // rank order, as all_reduce_sum (collectives.cpp:62-68)
+          if (pos >= a.xcap) {  // spilled: pull every source's value, rank order
+            for (int rr = 0; rr < n; ++rr) {
+              const T v = ld_relaxed_sys_t<T>(static_cast<const T*>(a.spill_peer[par][rr]) + pos);
+              sv[q] = rr == 0 ? v : sv[q] + v;
+            }
+          } else if (sums) {  // rank order, as all_reduce_sum (collectives.cpp:62-68)
             for (int rr = 0; rr < n; ++rr) {
               const T v = poll_ll<T>(static_cast<const unsigned long long*>(a.contrib_in[par][rr]) +
                                          pos * W, ep, a.err);

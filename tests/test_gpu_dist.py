@@ -112,3 +112,21 @@ def test_four_ranks_two_pass_exchange_holder_sum():
     _run(4, "--sync", "p2p", "--steps", "10", "--density", "0.05", port=29596,
          env={"EXD_TWO_PASS": "1"})
     _run(4, "--sync", "p2p", "--n_g", "20000003", "--steps", "5", "--skew", "0", port=29597)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("holder_sum", ["0", "1"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_two_ranks_bounded_inbox_spills_to_pull(holder_sum, dtype):
+    # contribution slots for 3000 union positions only (EXD_PUSH_CAP): the rest
+    # of every step's union goes through the sources' spill buffers and flags
+    _run(2, "--sync", "p2p", "--dtype", dtype, "--steps", "10",
+         port=29600 + 2 * (dtype == "f64") + int(holder_sum),
+         env={"EXD_PUSH_CAP": "3000", "EXD_HOLDER_SUM": holder_sum})
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_bounded_inbox_spills_to_pull():
+    _run(4, "--sync", "p2p", "--steps", "10", port=29604, env={"EXD_PUSH_CAP": "3000"})
+    _run(4, "--sync", "p2p", "--steps", "6", "--density", "0.1", port=29605,
+         env={"EXD_PUSH_CAP": "100000", "EXD_HOLDER_SUM": "0"})
