@@ -191,7 +191,7 @@ struct Worker {
   void* e = nullptr;
   int32_t* idx = nullptr;
   void* val = nullptr;
-  int32_t* blk = nullptr;             // 2 x n_b (double-buffered by step parity)
+  int32_t* blk = nullptr;             // n_b: per-block counts, computed on demand
   void* stage = nullptr;              // warp-chunk staging of the compaction ((idx, val) pairs)
   int32_t* chunk_count = nullptr;
   int32_t* tile_count = nullptr;
@@ -439,7 +439,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
     if (int r = alloc_zero(&wk.e, h->esz * ng)) return r;
     if (int r = alloc_zero((void**)&wk.idx, 4 * (size_t)h->cap_part)) return r;
     if (int r = alloc_zero(&wk.val, h->esz * (size_t)h->cap_part)) return r;
-    if (int r = alloc_zero((void**)&wk.blk, 4 * 2 * (size_t)cfg.n_b)) return r;
+    if (int r = alloc_zero((void**)&wk.blk, 4 * (size_t)cfg.n_b)) return r;
     // runs are placed at their first element's global index (stream kernel)
     const size_t stage_cap = ng + 2 * (size_t)h->tile;
     if (int r = alloc_zero(&wk.stage, 2 * h->esz * stage_cap)) return r;
@@ -845,8 +845,6 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.x = wk.x;
   a.idx = wk.idx;
   a.val = wk.val;
-  a.blk_counts = wk.blk + (h->t & 1) * h->cfg.n_b;
-  a.blk_next = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;
   a.stage = wk.stage;
   a.chunk_count = wk.chunk_count;
   a.tile_count = wk.tile_count;
@@ -1044,7 +1042,6 @@ int enqueue_step(exd_engine* h, const void* const* grads) {
       ca.idx = wk.idx;
       ca.val = wk.val;
       ca.e = wk.e;
-      ca.blk_counts = wk.blk + (h->t & 1) * c.n_b;
       ca.cnt = wk.cnt;
       ca.ctrl = wk.ctrl;
       ca.push = h->p2p ? h->d_push : nullptr;
@@ -1652,7 +1649,13 @@ int vector_of(exd_engine* h, int32_t w, int32_t which, const void** src, int64_t
     }
     case EXD_VEC_BLOCK_COUNTS:
       *n_el = h->cfg.n_b;
-      *src = wk.blk + ((h->t + 1) & 1) * h->cfg.n_b;  // parity of the last step
+      // counted on demand from the worker's own selection of the last step
+      if (h->has_record && !h->baseline)
+        CU(launch_block_counts(wk.idx, wk.cnt, h->cap_part, wk.blk, wk.rc, h->stream));
+      else
+        CU(cudaMemsetAsync(wk.blk, 0, 4 * (size_t)h->cfg.n_b, h->stream));
+      CU(cudaStreamSynchronize(h->stream));
+      *src = wk.blk;
       es = 4;
       break;
     case EXD_VEC_SUM:

@@ -89,8 +89,6 @@ struct SelectArgs {
   void* x;                  // T[n_g]   model (fused n == 1 only)
   int32_t* idx;             // [cap]    own selection, ascending
   void* val;                // T[cap]   own selected values
-  int32_t* blk_counts;      // [n_b]    per-block selection counts
-  int32_t* blk_next;        // [n_b]    block counters of step t + 1 (zeroed by the finish kernel)
   void* stage;              // [cap + 2 tiles] (index, value) pairs: warp-chunk staging runs
   int32_t* chunk_count;     // [tiles * kChunksPerTile] selected per warp chunk
   int32_t* tile_count;      // [tiles + 4] selected per tile (<= tile size)
@@ -242,12 +240,14 @@ cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void
                                       const void* xw, int64_t n_g, int dtype, int32_t w,
                                       uint32_t* flag, cudaStream_t s);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
+// per-block counts of a worker's own selection (EXD_VEC_BLOCK_COUNTS), on demand
+cudaError_t launch_block_counts(const int32_t* idx, const CountRec* cnt, int64_t cap, int32_t* out,
+                                RunConst rc, cudaStream_t s);
 // density cap (selector.cpp:44-61) on the compacted own selection
 struct CapArgs {
   int32_t* idx;                  // [k_i] own selection, ascending (compacted in place)
   void* val;                     // [k_i] own values (T)
   void* e;                       // residual: dropped elements get their acc back
-  int32_t* blk_counts;           // per-block counts of this step
   CountRec* cnt;                 // own {k_i, norm2, capped}
   Ctrl* ctrl;
   int32_t* const* push;          // P2P: [npush] my list slot in every peer's inbox

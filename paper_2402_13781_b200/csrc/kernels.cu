@@ -486,9 +486,6 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     // chunk that straddles a partition boundary never overlap (the peers'
     // inboxes keep one staging slot for all sources)
     const uint32_t sbase = lo;
-    const uint32_t hi = (cbeg + CH < end ? cbeg + CH : end) - 1;
-    const uint32_t b_lo = block_of(lo, rc), b_hi = block_of(hi, rc);
-    const bool split = b_lo != b_hi;
     uint64_t keep;
     if (a.stage_keep)
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
@@ -513,18 +510,12 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
             Pair<T>::store_keep(&sp[sbase + pos], Pair<T>::make(j, v[u][c]), keep);
 #endif
             spw[pos] = Pair<T>::make(j, v[u][c]);
-#ifndef EXD_XP_NO_BLK
-            if (split) atomicAdd(&a.blk_counts[block_of(j, rc)], 1);
-#endif
             ++pos;
           }
         }
       }
       running += (int)(__popc(b0) + 2u * __popc(b1) + 4u * __popc(b2));
     }
-#ifndef EXD_XP_NO_BLK
-    if (lane == 0 && !split && running) atomicAdd(&a.blk_counts[b_lo], running);
-#endif
     if (running) {
       __syncwarp();
 #ifndef EXD_XP_DIRECT_PAIR
@@ -694,8 +685,6 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SelectArgs a, RunConst
     __shared__ EpiShared esh;
     if (FUSED) epi_load(esh, ctrl);  // the stream kernel never writes the control block
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // next step's block counters (nobody reads that parity during this step)
-    for (int i = tid; i < rc.n_b; i += kThreads) a.blk_next[i] = 0;
     // one round of wide independent loads for both totals
     const int nt = (int)((n_g + TILE - 1) / TILE);
     double pn = 0.0;
@@ -1498,7 +1487,6 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     epi_load(esh, ctrl);  // the stream kernel never writes the control block
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) PROBE(0);
-    for (int i = tid; i < rc.n_b; i += kThreads) sa.blk_next[i] = 0;
     const int nt = (int)((rc.n_g + TILE - 1) / TILE);
     double pn = 0.0;
     int64_t pk = 0;
@@ -2097,7 +2085,6 @@ __global__ void __launch_bounds__(kCapThreads) cap_kernel(CapArgs a, RunConst rc
       for (int p = 0; p < a.npush; ++p) a.push[p][o] = j;
     } else if (i < ki) {
       e[j] = v;  // not in the union: the residual keeps acc (selector.cpp:63-65)
-      atomicAdd(&a.blk_counts[block_of((uint32_t)j, rc)], -1);
     }
     ties_before += ttot;
     out += ktot;
@@ -2641,6 +2628,41 @@ cudaError_t launch_quantile(const void* v, int64_t m, int64_t pos, int dtype, vo
     return quantile_t<double>(static_cast<const double*>(v), m, pos, q,
                               static_cast<double*>(out_bits), s);
   return quantile_t<float>(static_cast<const float*>(v), m, pos, q, static_cast<float*>(out_bits), s);
+}
+
+// Per-ExDyna-block selection counts of the last step (a diagnostic: the
+// reference keeps only per-partition counts, Appendix A of SURVEY.md), from the
+// worker's own ascending selection on demand. Counting them in the stream
+// kernel cost 40-55 us per step at n_g = 1e8: every warp of a wave added into
+// the same few block counters.
+__global__ void __launch_bounds__(256) block_counts_kernel(const int32_t* idx, const CountRec* cnt,
+                                                           int32_t* out, RunConst rc) {
+  extern __shared__ int32_t s_h[];
+  const bool smem = rc.n_b <= 8192;
+  if (smem)
+    for (int b = threadIdx.x; b < rc.n_b; b += blockDim.x) s_h[b] = 0;
+  __syncthreads();
+  const int64_t k = cnt->k;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = block_of((uint32_t)idx[i], rc);
+    if (smem) atomicAdd(&s_h[b], 1);
+    else atomicAdd(&out[b], 1);
+  }
+  __syncthreads();
+  if (smem)
+    for (int b = threadIdx.x; b < rc.n_b; b += blockDim.x)
+      if (s_h[b]) atomicAdd(&out[b], s_h[b]);
+}
+
+cudaError_t launch_block_counts(const int32_t* idx, const CountRec* cnt, int64_t cap, int32_t* out,
+                                RunConst rc, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int32_t) * (size_t)rc.n_b, s);
+  if (e != cudaSuccess) return e;
+  const int blocks = grid_for(cap > 0 ? cap : 1, 256 * 4);
+  const size_t sm = rc.n_b <= 8192 ? sizeof(int32_t) * (size_t)rc.n_b : 0;
+  block_counts_kernel<<<blocks, 256, sm, s>>>(idx, cnt, out, rc);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_verify_replication(const Ctrl* c0, const Ctrl* cw, const void* x0,
