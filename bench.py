@@ -518,6 +518,24 @@ def variants(S, torch, wl, local, budget_s, stream_ptr):
     return out
 
 
+def pin_to_gpu_cpus(index):
+    """Run this process on the CPUs local to GPU `index` (NVML affinity), so the
+    pinned host buffers of the e2e leg are first touched on the GPU's NUMA node."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -531,6 +549,7 @@ def run_ours(args):
     n = wl.n
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    cpus = pin_to_gpu_cpus(local)
     torch.cuda.set_device(local)
     dist = None
     if n > 1:
@@ -762,7 +781,9 @@ def run_ours(args):
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": es * N_G * n,
-                "d2h_bytes_per_step": C.sizeof(A.exd_record) * n},
+                "d2h_bytes_per_step": C.sizeof(A.exd_record) * n,
+                "h2d_gbs": es * N_G / (e2e_ms * 1e-3) / 1e9,
+                "host_cpus": f"{len(cpus)} GPU-local CPUs (NVML affinity)" if cpus else "unpinned"},
         "gpu_launches": launches,
         "nvlink": nvlink,
         "clocks": clk,

@@ -364,9 +364,7 @@ int setup(exd_engine* h, const exd_config* raw, const exd_options* opt, int firs
   // engine.cpp:58-61
   if (opt->sparsifier == EXD_SPARSIFIER_HARD_THRESHOLD && !(opt->fixed_delta > 0.0))
     return set_err(EXD_EINVAL, "fixed_delta out of range");
-  if (opt->sparsifier != EXD_SPARSIFIER_EXDYNA && h->dist && cfg.n > 1)
-    return set_err(EXD_EUNSUPPORTED,
-                   "the baseline sparsifiers run with in-process workers (exd_engine_create)");
+
   if (opt->dtype != EXD_F32 && opt->dtype != EXD_F64) return set_err(EXD_EINVAL, "dtype out of range");
   h->cfg = cfg;
   h->opt = *opt;
@@ -948,16 +946,56 @@ int enqueue_baseline_step(exd_engine* h, const void* const* grads) {
     h->stats.kernel_launches += 1;
   }
   std::vector<const int32_t*> lists(n);
-  for (int i = 0; i < nl; ++i) lists[i] = h->w[i].idx;
   int32_t* uni = h->w[0].idx_global;
-  CU(launch_baseline_union(lists.data(), h->counts_all, n, h->cap_part, c.n_g, h->bl_union, uni,
+  int64_t list_cap = h->cap_part, kp_host = 0;
+  if (h->dist && n > 1) {
+    // one rank per GPU (NCCL): the counts all-gather, one host wait for the
+    // padded list size (all_gather, collectives.cpp:22-57), the padded lists
+    Worker& wk = h->w[0];
+    NC(nccl().AllGather(wk.cnt, h->counts_all, sizeof(CountRec), ncclUint8, h->comm, h->stream));
+    CU(cudaMemcpyAsync(h->counts_host, h->counts_all, sizeof(CountRec) * n, cudaMemcpyDeviceToHost,
+                       h->stream));
+    if (int rc = wait_stream(h)) return rc;
+    int64_t m_t = 0;
+    for (int r = 0; r < n; ++r) {
+      m_t = std::max<int64_t>(m_t, h->counts_host[r].k);
+      kp_host += h->counts_host[r].k;
+    }
+    if (m_t * n > h->recv_cap) {
+      cudaFree(h->recv);
+      h->recv_cap = m_t * n + (m_t * n) / 4 + 1024;
+      CU(cudaMalloc((void**)&h->recv, 4 * (size_t)h->recv_cap));
+    }
+    if (m_t > 0)
+      NC(nccl().AllGather(wk.idx, h->recv, (size_t)m_t, ncclInt32, h->comm, h->stream));
+    for (int r = 0; r < n; ++r) lists[r] = h->recv + (size_t)r * m_t;
+    list_cap = m_t > 0 ? m_t : 1;
+  } else {
+    for (int i = 0; i < nl; ++i) lists[i] = h->w[i].idx;
+  }
+  CU(launch_baseline_union(lists.data(), h->counts_all, n, list_cap, c.n_g, h->bl_union, uni,
                            h->bl_ucnt, h->stream));
   h->stats.kernel_launches += baseline_union_launches(n);
-  for (int i = 0; i < nl; ++i) {
-    CU(launch_baseline_gather_clear(uni, h->bl_ucnt, h->w[i].e, h->w[i].contrib, c.n_g,
-                                    h->opt.dtype, h->stream));
+  if (h->dist && n > 1) {
+    // own contributions at the union, NCCL sum over the k' (>= |union|)
+    // entries the host knows (zero past the union: the NCCL order differs
+    // from rank order, as on the ExDyna NCCL path)
+    Worker& wk = h->w[0];
+    if (kp_host > 0) {
+      CU(cudaMemsetAsync(wk.contrib, 0, h->esz * (size_t)kp_host, h->stream));
+      CU(launch_baseline_gather_clear(uni, h->bl_ucnt, wk.e, wk.contrib, kp_host, h->opt.dtype,
+                                      h->stream));
+      NC(nccl().AllReduce(wk.contrib, h->sum, (size_t)kp_host,
+                          h->opt.dtype == EXD_F64 ? ncclFloat64 : ncclFloat32, ncclSum, h->comm,
+                          h->stream));
+    }
+  } else {
+    for (int i = 0; i < nl; ++i) {
+      CU(launch_baseline_gather_clear(uni, h->bl_ucnt, h->w[i].e, h->w[i].contrib, c.n_g,
+                                      h->opt.dtype, h->stream));
+    }
+    CU(launch_baseline_sum(h->d_contribs, n, h->bl_ucnt, h->sum, c.n_g, h->opt.dtype, h->stream));
   }
-  CU(launch_baseline_sum(h->d_contribs, n, h->bl_ucnt, h->sum, c.n_g, h->opt.dtype, h->stream));
   const double delta_used = sp == EXD_SPARSIFIER_HARD_THRESHOLD ? h->opt.fixed_delta : 0.0;
   for (int i = 0; i < nl; ++i) {
     Worker& wk = h->w[i];
@@ -1528,7 +1566,10 @@ int exd_engine_create_rank(const exd_config* cfg, const exd_options* opt, int32_
       cudaSetDevice(device);
       ncclResult_t r = nc.CommInitRank(&h->comm, cfg->n, id, rank);
       if (r != ncclSuccess) rc = set_err(EXD_ENCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
-      if (!rc && opt->sync_mode != EXD_SYNC_NCCL) rc = setup_p2p(h);
+      // the baseline sparsifiers' overlapping lists go through NCCL (all-gather +
+      // deduplicating union on every rank); ExDyna uses the peer-memory sync
+      if (!rc && opt->sync_mode != EXD_SYNC_NCCL && opt->sparsifier == EXD_SPARSIFIER_EXDYNA)
+        rc = setup_p2p(h);
     }
   }
   if (rc) {

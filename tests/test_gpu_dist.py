@@ -130,3 +130,17 @@ def test_four_ranks_bounded_inbox_spills_to_pull():
     _run(4, "--sync", "p2p", "--steps", "10", port=29604, env={"EXD_PUSH_CAP": "3000"})
     _run(4, "--sync", "p2p", "--steps", "6", "--density", "0.1", port=29605,
          env={"EXD_PUSH_CAP": "100000", "EXD_HOLDER_SUM": "0"})
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("kind", ["topk", "cltk", "hardthreshold"])
+def test_two_ranks_baseline_sparsifiers_over_nccl(kind):
+    # one rank per GPU: counts and padded lists all-gathered over NCCL, the
+    # deduplicating union on every rank, NCCL sum (exact at n = 2)
+    _run(2, "--sparsifier", kind, "--steps", "8", port=29610 + ["topk", "cltk", "hardthreshold"].index(kind))
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+def test_four_ranks_baseline_sparsifiers_over_nccl():
+    _run(4, "--sparsifier", "topk", "--steps", "6", port=29613)
+    _run(4, "--sparsifier", "cltk", "--steps", "6", "--dtype", "f64", port=29614)

@@ -28,6 +28,10 @@ def main():
     ap.add_argument("--sync", default="auto", choices=["auto", "nccl", "p2p", "p2p-pull"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--cap", type=float, default=None, help="max_density_cap")
+    ap.add_argument("--sparsifier", default="exdyna",
+                    choices=["exdyna", "topk", "cltk", "hardthreshold"],
+                    help="baseline sparsifiers run over NCCL, checked against oracle.BaselineOracle")
+    ap.add_argument("--fixed", type=float, default=2.2, help="hard threshold's fixed_delta")
     ap.add_argument("--kill-peer", type=int, default=0,
                     help="rank 1 stalls after 2 steps; rank 0's next steps must fail with the "
                          "engine's collective error (EXD_ENCCL) instead of hanging")
@@ -52,14 +56,24 @@ def main():
               max_density_cap=args.cap)
     ids = [S.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
-    eng = S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype=args.dtype, sync=args.sync),
+    base = args.sparsifier != "exdyna"
+    eng = S.Engine.rank(S.SparsifierConfig(**kw),
+                        S.EngineOptions(dtype=args.dtype, sync=args.sync, sparsifier=args.sparsifier,
+                                        fixed_delta=args.fixed if args.sparsifier == "hardthreshold" else 0.0),
                         rank, local, ids[0])
     segs = O.skew_segments(args.n_g) if args.skew else None
     src = S.SyntheticStream(S.StreamSpec(n_g=args.n_g, segments=segs, seed=5))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     buf = torch.empty(args.n_g, dtype=tdt, device=f"cuda:{local}")
-    orc = O.OracleEngine(O.make_config(**kw), np.float32 if args.dtype == "f32" else np.float64) \
-        if rank == 0 else None
+    ndt = np.float32 if args.dtype == "f32" else np.float64
+    if rank != 0:
+        orc = None
+    elif base:
+        orc = O.BaselineOracle(world, args.n_g, S.validate(S.SparsifierConfig(**kw)).k,
+                               args.sparsifier, args.fixed if args.sparsifier == "hardthreshold" else 0.0,
+                               dtype=ndt)
+    else:
+        orc = O.OracleEngine(O.make_config(**kw), ndt)
     tmp = torch.empty(args.n_g, dtype=tdt, device=f"cuda:{local}")
     ok = True
     if args.kill_peer:
@@ -124,9 +138,9 @@ def main():
                 torch.cuda.synchronize()
                 host.append(tmp.cpu().numpy().copy())
             orec = orc.step(host)
-            o = O.A.record_dict(orec)
+            o = orec if base else O.A.record_dict(orec)
             for f in ("k_prime", "m_t", "c_t", "f_t", "delta", "density", "eps", "adjust_moves",
-                      "adjust_skips", "union_count", "cap_hits"):
+                      "adjust_skips", "union_count", "cap_hits", "duplicates", "idle_workers"):
                 if getattr(rec, f) != o[f]:
                     print(f"[rank0] t={t} {f}: gpu={getattr(rec, f)} oracle={o[f]}", flush=True)
                     ok = False
@@ -136,26 +150,33 @@ def main():
             if abs(rec.global_err - o["global_err"]) > 1e-6 * max(o["global_err"], 1e-300):
                 print(f"[rank0] t={t} global_err {rec.global_err} vs {o['global_err']}", flush=True)
                 ok = False
-            if not np.array_equal(eng.idx_global().astype(np.int64), orc.union()):
+            if not np.array_equal(eng.idx_global().astype(np.int64),
+                                  orc.last_union if base else orc.union()):
                 print(f"[rank0] t={t} union differs", flush=True)
                 ok = False
     st = eng.state(0)
     mine = {"x": eng.x(0), "e": eng.e(0), "delta": st.delta, "k_t": list(st.k_t[:world]),
-            "parts": st.topology.parts(), "sel": eng.selection(0)}
+            "parts": st.topology.parts(), "sel": None if base else eng.selection(0)}
     allst = [None] * world
     dist.all_gather_object(allst, mine)
     if rank == 0:
         for r, m in enumerate(allst):
-            ost = orc.state(r)
-            if m["delta"] != ost.delta or m["k_t"] != list(ost.k_t[:world]) or \
-                    m["parts"] != ost.topology.parts():
-                print(f"[rank0] rank {r} control state differs", flush=True)
+            if base:
+                if m["k_t"] != list(orc.k_t):
+                    print(f"[rank0] rank {r} k_t differs", flush=True)
+                    ok = False
+                oe, ox = orc.e[r], orc.x[r]
+            else:
+                ost = orc.state(r)
+                if m["delta"] != ost.delta or m["k_t"] != list(ost.k_t[:world]) or \
+                        m["parts"] != ost.topology.parts():
+                    print(f"[rank0] rank {r} control state differs", flush=True)
+                    ok = False
+                oe, ox = orc.e(r), orc.x(r)
+            if not np.array_equal(m["e"], oe):
+                print(f"[rank0] rank {r} residual differs ({int(np.sum(m['e'] != oe))})", flush=True)
                 ok = False
-            if not np.array_equal(m["e"], orc.e(r)):
-                print(f"[rank0] rank {r} residual differs ({int(np.sum(m['e'] != orc.e(r)))})", flush=True)
-                ok = False
-            ox = orc.x(r)
-            if world <= 2 or args.sync != "nccl":
+            if world <= 2 or (args.sync != "nccl" and not base):
                 # the peer-memory sync sums in rank order like the reference
                 same = np.array_equal(m["x"], ox)
             else:
@@ -164,10 +185,10 @@ def main():
             if not same:
                 print(f"[rank0] rank {r} x differs (max {np.max(np.abs(m['x'] - ox))})", flush=True)
                 ok = False
-            if not np.array_equal(m["sel"].astype(np.int64), orc.selection(r)):
+            if not base and not np.array_equal(m["sel"].astype(np.int64), orc.selection(r)):
                 print(f"[rank0] rank {r} selection differs", flush=True)
                 ok = False
-        print(f"dist_check world={world} sync={args.sync} ({eng.sync_mode()}) dtype={args.dtype} cap={args.cap} n_g={args.n_g} steps={args.steps}: "
+        print(f"dist_check world={world} sparsifier={args.sparsifier} sync={args.sync} ({eng.sync_mode()}) dtype={args.dtype} cap={args.cap} n_g={args.n_g} steps={args.steps}: "
               f"{'PASS' if ok else 'FAIL'} (last k'={rec.k_prime} f_t={rec.f_t:.3f})", flush=True)
     flag = torch.tensor([1 if ok else 0])
     dist.broadcast(flag, src=0)
