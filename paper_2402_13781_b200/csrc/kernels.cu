@@ -351,9 +351,8 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
   static_assert(CH * kWarps == tile_of<T>(), "tile = kWarps chunks");
   __shared__ double s_norm[kWarps];
   __shared__ int s_cnt[kWarps];
-  // each warp's run of (index, value) pairs, compacted here and then written
-  // to the staging buffer (and, PUSH, to the peers) with coalesced stores
-  __shared__ typename Pair<T>::P s_pair[SELECT ? kWarps * CH : 1];
+  // PUSH: each warp's run of staged indices, copied to the peers coalesced
+  __shared__ int32_t s_run[PUSH ? kWarps * CH : 1];
 
   const Ctrl* ctrl = a.ctrl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -492,7 +491,6 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     else
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(keep));
     typename Pair<T>::P* sp = static_cast<typename Pair<T>::P*>(a.stage);
-    typename Pair<T>::P* spw = s_pair + warp * CH;  // this warp's run, compacted
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t nib = (flags >> (u * VN)) & ((1u << VN) - 1u);
@@ -506,33 +504,25 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
         for (int c = 0; c < VN; ++c) {
           if ((nib >> c) & 1u) {
             const uint32_t j = lbeg + u * 32 * VN + c;
-#ifdef EXD_XP_DIRECT_PAIR
+            // straight to the staging buffer (measured faster than compacting
+            // through shared memory first: 24.0 vs 27.6 us at R18)
             Pair<T>::store_keep(&sp[sbase + pos], Pair<T>::make(j, v[u][c]), keep);
-#endif
-            spw[pos] = Pair<T>::make(j, v[u][c]);
+            if (PUSH) s_run[warp * CH + pos] = (int32_t)j;
             ++pos;
           }
         }
       }
       running += (int)(__popc(b0) + 2u * __popc(b1) + 4u * __popc(b2));
     }
-    if (running) {
+    if (PUSH && running) {
+      // the run sbase + [0, running) in every peer's staging slot as
+      // {index, epoch} words: 256 B coalesced stores, each word its own flag
       __syncwarp();
-#ifndef EXD_XP_DIRECT_PAIR
-      // the run sbase + [0, running) with coalesced stores: a warp instruction
-      // writes 32 consecutive pairs (the finish / exchange kernels read them
-      // right after the stream: kept in L2 past the streaming data when small)
-      for (int i = lane; i < running; i += 32) Pair<T>::store_keep(&sp[sbase + i], spw[i], keep);
-#endif
-      if (PUSH) {
-        // and in every peer's staging slot as {index, epoch} words: 256 B
-        // coalesced stores, each word its own flag
-        const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
-        for (int q = 0; q < a.k1_npush; ++q) {
-          unsigned long long* dst = a.push_stage[q] + sbase;
-          for (int i = lane; i < running; i += 32)
-            st_relaxed_sys_u64(dst + i, eph | Pair<T>::idx(spw[i]));
-        }
+      const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
+      for (int q = 0; q < a.k1_npush; ++q) {
+        unsigned long long* dst = a.push_stage[q] + sbase;
+        for (int i = lane; i < running; i += 32)
+          st_relaxed_sys_u64(dst + i, eph | (uint32_t)s_run[warp * CH + i]);
       }
     }
   }
