@@ -312,10 +312,14 @@ int wait_stream(exd_engine* h) {
     if (e == cudaSuccess) return EXD_OK;
     if (e != cudaErrorNotReady)
       return set_err(EXD_ECUDA, std::string("engine stream: ") + cudaGetErrorString(e));
-    ncclResult_t ar = ncclSuccess;
-    nccl().CommGetAsyncError(h->comm, &ar);
+    // spin for the first ~50 ms (a sleeping host wakes late and every peer's
+    // kernel then waits for this rank's next step); check the communicator
+    // every 1024 polls, then poll at 50 us
     const double el =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el < 0.05 && (spin & 1023u) != 1023u) continue;
+    ncclResult_t ar = ncclSuccess;
+    nccl().CommGetAsyncError(h->comm, &ar);
     if ((ar != ncclSuccess && ar != ncclInProgress) || el > nccl_timeout_s()) {
       const std::string why =
           ar != ncclSuccess && ar != ncclInProgress
@@ -327,7 +331,7 @@ int wait_stream(exd_engine* h) {
       h->broken = true;
       return set_err(EXD_ENCCL, why);
     }
-    if (spin > 1000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    if (el >= 0.05) std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
 }
 

@@ -1864,8 +1864,8 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         __syncthreads();  // the block's spill stores, before the fence
         if (tid == 0) {
           asm volatile("fence.acq_rel.sys;" ::: "memory");
-          for (int rr = 0; rr < n; ++rr)
-            if (rr != me) st_relaxed_sys_u64(a.spill_flag_out[par][rr] + r, ep);
+          for (int rr = 0; rr < n; ++rr)  // {0, epoch}: poll_word matches the high half
+            if (rr != me) st_relaxed_sys_u64(a.spill_flag_out[par][rr] + r, (unsigned long long)ep << 32);
           for (int rr = 0; rr < n; ++rr)
             if (rr != me) poll_word(a.spill_flag_in[par] + (size_t)rr * kMaxCtas + r, ep, a.err);
           asm volatile("fence.acq_rel.sys;" ::: "memory");
