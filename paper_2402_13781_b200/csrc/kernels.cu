@@ -516,13 +516,21 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
     }
     if (PUSH && running) {
       // the run sbase + [0, running) in every peer's staging slot as
-      // {index, epoch} words: 256 B coalesced stores, each word its own flag
+      // {index, epoch} words, each word its own flag: 16 B stores of two words
+      // (512 B per warp instruction; a leading word when sbase is odd)
       __syncwarp();
       const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
+      const int32_t* run = s_run + warp * CH;
+      const int h0 = (int)(sbase & 1u);  // words before the first 16 B boundary
       for (int q = 0; q < a.k1_npush; ++q) {
         unsigned long long* dst = a.push_stage[q] + sbase;
-        for (int i = lane; i < running; i += 32)
-          st_relaxed_sys_u64(dst + i, eph | (uint32_t)s_run[warp * CH + i]);
+        if (h0 && lane == 0) st_relaxed_sys_u64(dst, eph | (uint32_t)run[0]);
+        for (int i = h0 + 2 * lane; i < running; i += 64) {
+          if (i + 1 < running)
+            st_relaxed_sys_v2u64(dst + i, eph | (uint32_t)run[i], eph | (uint32_t)run[i + 1]);
+          else
+            st_relaxed_sys_u64(dst + i, eph | (uint32_t)run[i]);
+        }
       }
     }
   }
