@@ -1413,7 +1413,7 @@ __device__ __forceinline__ T poll_ll(const unsigned long long* w, uint32_t ep, u
 }
 
 constexpr int kXUnroll = 4;   // union entries per thread in flight
-constexpr int kX2Unroll = 4;  // pass-2 positions per thread in flight (TWO)
+constexpr int kX2Unroll = 8;  // pass-2 positions per thread in flight (TWO)
 constexpr int kXPeers = 4;    // peer words per entry polled together
 
 // TWO (large k'): the work loop runs in two passes per block, so no NVLink
@@ -1685,11 +1685,21 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
     cnt = (int)(uint32_t)cw;
     PROBE_MAX(41);
     int64_t running = base;  // union position of tile t0's first entry
+    unsigned long long cw_next = (unsigned long long)ep << 32;  // BIG: next batch's count word
     for (int cb = 0; cb < nch; cb += kThreads) {
       const int nb = nch - cb < kThreads ? nch - cb : kThreads;
       if (cb) {
         cnt = 0;
-        if (tid < nb) cnt = (int)poll_word(&ccnt_ll[t0 * kWarps + cb + tid], ep, a.err);
+        if (tid < nb) {
+          const unsigned long long* wp = &ccnt_ll[t0 * kWarps + cb + tid];
+          cnt = BIG && (uint32_t)(cw_next >> 32) == ep ? (int)(uint32_t)cw_next
+                                                         : (int)poll_word(wp, ep, a.err);
+        }
+      }
+      if (BIG) {  // issue the next batch's count words now: in flight during this batch
+        const int cn = cb + kThreads + tid;
+        cw_next = cn < nch ? ld_relaxed_sys_u64(&ccnt_ll[t0 * kWarps + cn])
+                           : (unsigned long long)ep << 32;
       }
       int incl = cnt;
 #pragma unroll
