@@ -1874,6 +1874,7 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
       __syncthreads();
     }
     if (TWO) {
+      PROBE_MAX(45);  // pass 1 done (probe builds)
       // spilled positions (past the contribution slots): publish this block's
       // spill writes to the peers, then wait for theirs (one flag per source
       // and block; every rank splits the union the same way)
