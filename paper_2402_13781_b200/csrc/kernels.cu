@@ -1570,6 +1570,10 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   // (this rank's own too), so the lookups below overlap this rank's stream
   // kernel draining its remote stores. The wait comes before the first access
   // to what the stream kernel writes locally (e, the staged values).
+  // Large vectors wait first: there the stream kernel runs for hundreds of us,
+  // and work blocks polling words all that time take issue slots and memory
+  // bandwidth from it (EXD_EARLY_POLL=1 keeps the early lookups).
+  if (BIG && !a.early_poll) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (r == 0) PROBE(8);
 
