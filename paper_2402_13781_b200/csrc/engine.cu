@@ -257,7 +257,6 @@ struct exd_engine {
   std::vector<unsigned long long*> spill_flag_out[2];  // [n] my flag row in every inbox
   unsigned long long* spill_flag_in[2] = {nullptr, nullptr};  // own flag area [n][kMaxCtas]
   int two_pass = -1;                  // exchange work loop: -1 by size, 0/1 forced (EXD_TWO_PASS)
-  bool early_poll = false;            // large vectors: exchange lookups before the wait (EXD_EARLY_POLL=1)
   int xchg_blocks = 444;              // exchange work blocks (3 per SM - 1)
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
@@ -789,7 +788,6 @@ int setup_p2p(exd_engine* h) {
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
   if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
   if (const char* tp = std::getenv("EXD_TWO_PASS")) h->two_pass = tp[0] == '1' ? 1 : 0;
-  if (const char* ep = std::getenv("EXD_EARLY_POLL")) h->early_poll = ep[0] == '1';
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -908,7 +906,6 @@ ExchangeArgs exchange_args(exd_engine* h, const SelectArgs& sa) {
   // (k entries over ~3 blocks per SM, 4 per thread in flight): two passes
   o.two_pass = h->two_pass >= 0 ? h->two_pass : (h->cfg.k > (int64_t)h->xchg_blocks * 4 * 256 ? 1 : 0);
   o.xcap = h->xcap;
-  o.early_poll = h->early_poll ? 1 : 0;
   if (h->xcap < h->cfg.n_g) {
     o.two_pass = 1;  // the spill pull lives in pass 2
     for (int par = 0; par < 2; ++par) {

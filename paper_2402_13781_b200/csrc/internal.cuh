@@ -209,7 +209,6 @@ struct ExchangeArgs {
   unsigned int* err;                 // set on a peer timeout (device memory)
   int32_t me;
   int32_t two_pass;                  // large k': the work loop in two passes (exchange_kernel)
-  int32_t early_poll;                // large vectors: look words up before griddepcontrol.wait too
   // bounded contribution slots: union positions >= xcap are not pushed; each
   // source writes them to its exported spill buffer, raises a per-block flag
   // in every peer's inbox, and the peers pull them (pass 2)

@@ -559,16 +559,24 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) sc += s_cnt[w];
       a.tile_count[tile] = sc;
-      if (push_tile) {
-        // the tile's kWarps chunk counts and its count as {count, epoch} words
-        const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
-        for (int q = 0; q < a.k1_npush; ++q) {
-          unsigned long long* d = a.push_chunk[q] + tile * kWarps;
+    }
+  }
+  if (push_tile && warp == 0) {
+    // the tile's kWarps chunk counts and its count as {count, epoch} words into
+    // every inbox: one store per lane (4 chunk-count pairs + the tile count per
+    // destination), not a serial loop on one thread
+    static_assert(kWarps == 8, "4 chunk-count pairs per tile");
+    int sc = 0;
 #pragma unroll
-          for (int w = 0; w < kWarps; w += 2) st_relaxed_sys_v2u64(d + w, eph | (uint32_t)s_cnt[w], eph | (uint32_t)s_cnt[w + 1]);
-          st_relaxed_sys_u64(a.push_tile[q] + tile, eph | (uint32_t)sc);
-        }
-      }
+    for (int w = 0; w < kWarps; ++w) sc += s_cnt[w];
+    const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
+    for (int l = lane; l < a.k1_npush * 5; l += 32) {
+      const int q = l / 5, i = l - 5 * q;
+      if (i < 4)
+        st_relaxed_sys_v2u64(a.push_chunk[q] + tile * kWarps + 2 * i, eph | (uint32_t)s_cnt[2 * i],
+                             eph | (uint32_t)s_cnt[2 * i + 1]);
+      else
+        st_relaxed_sys_u64(a.push_tile[q] + tile, eph | (uint32_t)sc);
     }
   }
   PROBE_MAX(31);
@@ -1570,10 +1578,6 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
   // (this rank's own too), so the lookups below overlap this rank's stream
   // kernel draining its remote stores. The wait comes before the first access
   // to what the stream kernel writes locally (e, the staged values).
-  // Large vectors wait first: there the stream kernel runs for hundreds of us,
-  // and work blocks polling words all that time take issue slots and memory
-  // bandwidth from it (EXD_EARLY_POLL=1 keeps the early lookups).
-  if (BIG && !a.early_poll) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (r == 0) PROBE(8);
 
