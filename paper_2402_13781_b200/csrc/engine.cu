@@ -257,6 +257,7 @@ struct exd_engine {
   std::vector<unsigned long long*> spill_flag_out[2];  // [n] my flag row in every inbox
   unsigned long long* spill_flag_in[2] = {nullptr, nullptr};  // own flag area [n][kMaxCtas]
   int two_pass = -1;                  // exchange work loop: -1 by size, 0/1 forced (EXD_TWO_PASS)
+  int tile_pack = 1;                  // K1 pushes its indices packed per tile (EXD_TILE_PACK)
   int xchg_blocks = 444;              // exchange work blocks (3 per SM - 1)
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
@@ -788,6 +789,7 @@ int setup_p2p(exd_engine* h) {
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
   if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
   if (const char* tp = std::getenv("EXD_TWO_PASS")) h->two_pass = tp[0] == '1' ? 1 : 0;
+  if (const char* tk = std::getenv("EXD_TILE_PACK")) h->tile_pack = tk[0] == '1' ? 1 : 0;
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -863,6 +865,7 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.k1_npush = h->xchg ? h->n : 0;  // every peer, then this rank's own inbox
   // pairs of ~2k/n selections (16 B fp64, 8 B fp32) against a 32 MB share of L2
   a.stage_keep = 2 * (double)h->cfg.k / h->n * (h->esz == 8 ? 16 : 8) < 32e6 ? 1 : 0;
+  a.tile_pack = h->tile_pack;
   a.range_words = wk.range_words;
   const int par = (int)(h->t & 1);  // this step's parity slots
   for (int q = 0; q < a.k1_npush; ++q) {

@@ -110,6 +110,8 @@ struct SelectArgs {
   int32_t k1_npush;             // 0: no pushes
   unsigned long long* range_words;  // finish kernel, large vectors: [3][kMaxCtas] published
                                     // range counts / ||e||^2 halves (nullptr: small vector)
+  int32_t tile_pack;            // PUSH: staged indices packed per tile (1) or pushed as
+                                // per-warp runs at the chunk's position (0)
   int32_t stage_keep;           // staged pairs small enough to keep in L2 (evict_last);
                                 // else streamed (evict_first) so they do not crowd the
                                 // 126 MB L2 at large k

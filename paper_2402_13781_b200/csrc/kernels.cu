@@ -4,8 +4,9 @@
 //                   |acc| >= delta over the worker's exclusive partition,
 //                   own selected residuals zeroed, the selection staged in
 //                   order per warp chunk as (index, value) pairs, per-block
-//                   counts. PUSH variant (one rank per GPU): the staged runs
-//                   and counts also go to every peer's inbox.
+//                   counts. PUSH variant (one rank per GPU): the staged
+//                   indices (packed per tile) and counts also go to every
+//                   peer's inbox.
 //   finish_kernel   (K2) per-chunk counts -> global offsets, dense ascending
 //                   idx/val lists; for n == 1 also x -= g/n and the control
 //                   epilogue, so a step is two launches chained by PDL.
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
   static_assert(CH * kWarps == tile_of<T>(), "tile = kWarps chunks");
   __shared__ double s_norm[kWarps];
   __shared__ int s_cnt[kWarps];
-  // PUSH: each warp's run of staged indices, copied to the peers coalesced
+  // PUSH: each warp's run of staged indices, packed per tile for the peers
   __shared__ int32_t s_run[PUSH ? kWarps * CH : 1];
 
   const Ctrl* ctrl = a.ctrl;
@@ -514,14 +515,14 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
       }
       running += (int)(__popc(b0) + 2u * __popc(b1) + 4u * __popc(b2));
     }
-    if (PUSH && running) {
+    if (PUSH && !a.tile_pack && running) {
       // the run sbase + [0, running) in every peer's staging slot as
       // {index, epoch} words, each word its own flag: 16 B stores of two words
-      // (512 B per warp instruction; a leading word when sbase is odd)
+      // (a leading word when sbase is odd)
       __syncwarp();
       const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
       const int32_t* run = s_run + warp * CH;
-      const int h0 = (int)(sbase & 1u);  // words before the first 16 B boundary
+      const int h0 = (int)(sbase & 1u);
       for (int q = 0; q < a.k1_npush; ++q) {
         unsigned long long* dst = a.push_stage[q] + sbase;
         if (h0 && lane == 0) st_relaxed_sys_u64(dst, eph | (uint32_t)run[0]);
@@ -559,6 +560,42 @@ __global__ void __launch_bounds__(kThreads, EXD_K1_MINB) stream_kernel(SelectArg
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) sc += s_cnt[w];
       a.tile_count[tile] = sc;
+    }
+  }
+  if (PUSH && a.tile_pack && s_cnt[0] + s_cnt[1] + s_cnt[2] + s_cnt[3] + s_cnt[4] + s_cnt[5] + s_cnt[6] +
+                   s_cnt[7] > 0) {
+    // the tile's staged indices, packed in chunk order, into every peer's inbox
+    // at max(tile start, partition start) as {index, epoch} words (each word
+    // its own flag): one contiguous burst per tile and destination. Per-warp
+    // runs of a few words each were bound by the NVLink request rate
+    // (tools/nvl_word_bench.cu: ~5 G short runs/s per GPU), not by bytes.
+    static_assert(kWarps == 8, "the packed offsets below sum 8 chunk counts");
+    int woff[kWarps], sc = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      woff[w] = sc;
+      sc += s_cnt[w];
+    }
+    const uint32_t t0 = (uint32_t)tile * TILE;
+    const uint32_t tb = t0 > st ? t0 : st;
+    const int h0 = (int)(tb & 1u);  // a leading single word when tb is odd
+    const unsigned long long eph = (unsigned long long)(uint32_t)(a.t + 1) << 32;
+    auto word = [&](int i) {
+      int w = 0;
+#pragma unroll
+      for (int k = 1; k < kWarps; ++k) w += woff[k] <= i;
+      return eph | (uint32_t)s_run[w * CH + (i - woff[w])];
+    };
+    for (int q = 0; q < a.k1_npush; ++q) {
+      unsigned long long* dst = a.push_stage[q] + tb;
+      for (int i = 2 * (int)threadIdx.x - h0; i < sc; i += 2 * kThreads) {
+        if (i < 0)
+          st_relaxed_sys_u64(dst, word(0));
+        else if (i + 1 < sc)
+          st_relaxed_sys_v2u64(dst + i, word(i), word(i + 1));
+        else
+          st_relaxed_sys_u64(dst + i, word(i));
+      }
     }
   }
   if (push_tile && warp == 0) {
@@ -1731,14 +1768,14 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
         int32_t jj[kXUnroll];
         T vv[kXUnroll];
         unsigned long long jw[kXUnroll];
-        int64_t src[kXUnroll];
+        int64_t src[kXUnroll], wsrc[kXUnroll];
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {
           const int i = i0 + q * kThreads;
           jj[q] = 0;
           vv[q] = T(0);
           jw[q] = (unsigned long long)ep << 32;
-          src[q] = 0;
+          src[q] = wsrc[q] = 0;
           if (i < btot) {
             int lo = 0, hi = nb;  // last chunk k with s_off[k] <= i
             while (hi - lo > 1) {
@@ -1747,12 +1784,17 @@ __global__ void __launch_bounds__(kThreads, 3) exchange_kernel(ExchangeArgs a, R
             }
             const int64_t cst = (cbase + lo) * CH;  // runs start at max(chunk, partition start)
             src[q] = (cst > pst ? cst : pst) + (i - s_off[lo]);
-            jw[q] = ld_relaxed_sys_u64(&sidx[src[q]]);
+            // the pushed words are packed per tile from max(tile start,
+            // partition start); batches start on tile boundaries (cbase % 8 == 0)
+            const int64_t tst = (cbase + lo) / kWarps * TILE;
+            wsrc[q] = sa.tile_pack ? (tst > pst ? tst : pst) + (i - s_off[lo & ~(kWarps - 1)])
+                                   : src[q];
+            jw[q] = ld_relaxed_sys_u64(&sidx[wsrc[q]]);
           }
         }
 #pragma unroll
         for (int q = 0; q < kXUnroll; ++q) {
-          if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[src[q]], ep, a.err);
+          if ((uint32_t)(jw[q] >> 32) != ep) jw[q] = poll_word(&sidx[wsrc[q]], ep, a.err);
           jj[q] = (int32_t)(uint32_t)jw[q];
         }
         // x is not written by the stream kernel (the previous step's kernels

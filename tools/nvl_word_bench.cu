@@ -22,9 +22,22 @@
 
 // mode 0: one 8 B word per thread per iteration (st.relaxed.sys.u64)
 // mode 1: two words per thread per iteration as one 16 B store (st.relaxed.sys.v2.u64)
-__global__ void push_words(unsigned long long* dst, long long nwords, unsigned ep, int mode) {
+// mode 2: short runs like the stream kernel's pushes: each warp writes `run`
+//         consecutive words at the start of every 512-word chunk it owns
+__global__ void push_words(unsigned long long* dst, long long nwords, unsigned ep, int mode,
+                           int run) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   const unsigned long long tag = (unsigned long long)ep << 32;
+  if (mode == 2) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = stride >> 5;
+    for (long long c = warp; c * 512 < nwords; c += nwarps)
+      if (lane < run)
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst + c * 512 + lane),
+                     "l"(tag | (unsigned)lane) : "memory");
+    return;
+  }
   if (mode == 0) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride)
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst + i), "l"(tag | (unsigned)i)
@@ -68,7 +81,7 @@ int main(int argc, char** argv) {
       float best = 1e30f;
       for (int rep = 0; rep < 6; ++rep) {
         CK(cudaEventRecord(a));
-        push_words<<<sms * per_sm, 256>>>(remote, nwords, rep + 1, mode);
+        push_words<<<sms * per_sm, 256>>>(remote, nwords, rep + 1, mode, 0);
         CK(cudaEventRecord(b));
         CK(cudaEventSynchronize(b));
         float ms = 0.f;
@@ -78,6 +91,32 @@ int main(int argc, char** argv) {
       std::printf("mode=%s blocks/SM=%d: %lld MB of words in %.3f ms = %.1f GB/s (%.1f%% of 770)\n",
                   mode ? "v2.u64 (16 B)" : "u64 (8 B)", per_sm, mb, best,
                   nwords * 8 / (best * 1e-3) / 1e9, nwords * 8 / (best * 1e-3) / 770e9 * 100);
+    }
+  }
+  // short runs: the same chunk grid, `run` words written per 512-word chunk
+  for (int run : {1, 5, 16, 32}) {
+    for (int local = 0; local < 2; ++local) {
+      unsigned long long* dst = remote;
+      unsigned long long* loc = nullptr;
+      if (local) {
+        CK(cudaMalloc(&loc, nwords * 8));
+        dst = loc;
+      }
+      float best = 1e30f;
+      for (int rep = 0; rep < 6; ++rep) {
+        CK(cudaEventRecord(a));
+        push_words<<<sms * 4, 256>>>(dst, nwords, rep + 1, 2, run);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (rep > 0 && ms < best) best = ms;
+      }
+      const double nruns = (double)(nwords / 512);
+      std::printf("runs of %2d words per 512-word chunk to %s: %.0f runs in %.3f ms = %.1f M runs/s, %.1f GB/s of words\n",
+                  run, local ? "LOCAL memory" : "the peer", nruns, best, nruns / (best * 1e-3) / 1e6,
+                  nruns * run * 8 / (best * 1e-3) / 1e9);
+      if (loc) cudaFree(loc);
     }
   }
   return 0;
