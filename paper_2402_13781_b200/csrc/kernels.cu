@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <atomic>
 
 #include "internal.cuh"
 
@@ -944,14 +945,20 @@ cudaError_t launch_stream_t(int mode, const SelectArgs& a, const RunConst& rc, c
   return cudaGetLastError();
 }
 
+constexpr int kMaxDevices = 64;
+
 template <typename T>
 cudaError_t launch_finish_t(const SelectArgs& a, const RunConst& rc, cudaStream_t s) {
-  static int cap = 0;
+  // copy-CTA cap per device (engines of one process may sit on different GPUs)
+  static std::atomic<int> caps[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int cap = dev < kMaxDevices ? caps[dev].load(std::memory_order_relaxed) : 0;
   if (cap == 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
+    int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cap = sms * EXD_COPY_PER_SM > kMaxCtas ? kMaxCtas : sms * EXD_COPY_PER_SM;
+    if (dev < kMaxDevices) caps[dev].store(cap, std::memory_order_relaxed);
   }
   // the partition's tile count is device-resident; size for the whole vector,
   // plus one epilogue CTA
