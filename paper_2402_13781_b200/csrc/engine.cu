@@ -257,7 +257,8 @@ struct exd_engine {
   std::vector<unsigned long long*> spill_flag_out[2];  // [n] my flag row in every inbox
   unsigned long long* spill_flag_in[2] = {nullptr, nullptr};  // own flag area [n][kMaxCtas]
   int two_pass = -1;                  // exchange work loop: -1 by size, 0/1 forced (EXD_TWO_PASS)
-  int tile_pack = 1;                  // K1 pushes its indices packed per tile (EXD_TILE_PACK)
+  int tile_pack = -1;                 // K1 pushes its indices packed per tile: -1 by size, 0/1
+                                      // forced (EXD_TILE_PACK)
   int xchg_blocks = 444;              // exchange work blocks (3 per SM - 1)
   void* p2p_own_contrib[2] = {nullptr, nullptr};  // own contribution buffers (parity)
   // push-reduce (EXD_SYNC_P2P without a cap): inbox = flags[2][n] | staged idx[2][n][stage_cap]
@@ -865,7 +866,11 @@ SelectArgs select_args(exd_engine* h, Worker& wk, const void* grad) {
   a.k1_npush = h->xchg ? h->n : 0;  // every peer, then this rank's own inbox
   // pairs of ~2k/n selections (16 B fp64, 8 B fp32) against a 32 MB share of L2
   a.stage_keep = 2 * (double)h->cfg.k / h->n * (h->esz == 8 ? 16 : 8) < 32e6 ? 1 : 0;
-  a.tile_pack = h->tile_pack;
+  // packed per tile on large vectors (fewer, longer NVLink bursts: 1e9 d = 0.001
+  // at N = 4 2.86 vs 3.00 ms); per-warp runs on small ones, where the step is
+  // latency-bound and a run leaves before its tile's barrier (R18 N = 4: 49.1 vs
+  // 49.6 us)
+  a.tile_pack = h->tile_pack >= 0 ? h->tile_pack : (h->tiles > kBaseRoundTiles ? 1 : 0);
   a.range_words = wk.range_words;
   const int par = (int)(h->t & 1);  // this step's parity slots
   for (int q = 0; q < a.k1_npush; ++q) {

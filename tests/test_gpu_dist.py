@@ -39,10 +39,10 @@ def test_two_ranks_push_reduce_holder_sum_switch(holder_sum):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-def test_two_ranks_push_reduce_per_warp_runs():
-    # the stream kernel's pushed indices as per-warp runs at the chunk's
-    # position instead of packed per tile (EXD_TILE_PACK=0), large vector too
-    _run(2, "--sync", "p2p", "--steps", "10", port=29615, env={"EXD_TILE_PACK": "0"})
+def test_two_ranks_push_reduce_index_layouts():
+    # the stream kernel pushes its indices packed per tile on large vectors and
+    # as per-warp runs at the chunk's position on small ones; force the other way
+    _run(2, "--sync", "p2p", "--steps", "10", port=29615, env={"EXD_TILE_PACK": "1"})
     _run(2, "--sync", "p2p", "--n_g", "20000003", "--steps", "5", "--skew", "0", port=29616,
          env={"EXD_TILE_PACK": "0"})
 
