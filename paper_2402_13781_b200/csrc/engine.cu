@@ -616,6 +616,43 @@ int setup_p2p(exd_engine* h) {
   // push-reduce unless the caller asked for pull-reduce, or a density cap /
   // verify_conservation needs the trimmed lists and contribution buffers first
   h->xchg = h->opt.sync_mode != EXD_SYNC_P2P_PULL && h->cap == 0 && !h->opt.verify_conservation;
+  // protocol switches: the peers' kernels read each other's inbox layout, so
+  // every rank must run the same ones (the environment is per process)
+  h->holder_sum = n >= 4;
+  if (const char* hs = std::getenv("EXD_HOLDER_SUM")) h->holder_sum = hs[0] == '1';
+  if (const char* tp = std::getenv("EXD_TWO_PASS")) h->two_pass = tp[0] == '1' ? 1 : 0;
+  if (const char* tk = std::getenv("EXD_TILE_PACK")) h->tile_pack = tk[0] == '1' ? 1 : 0;
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->xchg_blocks = 3 * sms - 1;  // the spill flags are indexed by work block
+  }
+  const char* push_cap_env = std::getenv("EXD_PUSH_CAP");
+  {
+    static const char* const kNames[] = {"sync mode / density cap / verify_conservation",
+                                         "EXD_HOLDER_SUM", "EXD_TWO_PASS", "EXD_TILE_PACK",
+                                         "EXD_PUSH_CAP", "SM count"};
+    constexpr int kN = 6;
+    int64_t v[2 * kN] = {h->xchg ? 1 : 0,
+                         h->holder_sum ? 1 : 0,
+                         h->two_pass,
+                         h->tile_pack,
+                         push_cap_env ? std::atoll(push_cap_env) : -1,
+                         h->xchg_blocks};
+    for (int i = 0; i < kN; ++i) v[kN + i] = -v[i];  // one min-reduce gives min and -max
+    int64_t* d_v = nullptr;
+    CU(cudaMalloc((void**)&d_v, sizeof(v)));
+    CU(cudaMemcpy(d_v, v, sizeof(v), cudaMemcpyHostToDevice));
+    NC(nccl().AllReduce(d_v, d_v, 2 * kN, ncclInt64, ncclMin, h->comm, h->stream));
+    int64_t r[2 * kN];
+    CU(cudaMemcpyAsync(r, d_v, sizeof(r), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    cudaFree(d_v);
+    for (int i = 0; i < kN; ++i)
+      if (r[i] != -r[kN + i])
+        return set_err(EXD_EINVAL, std::string("peer-memory sync: ") + kNames[i] +
+                                       " differs across ranks; every rank must use the same");
+  }
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   size_t flags_b = 0, list_b = 0, con_b = 0, off_lists = 0, off_c0 = 0, off_c1 = 0, total = 0;
   size_t stage_b = 0, chunk_b = 0, tile_b = 0, xcon_b = 0, off_st = 0, off_ch = 0, off_ti = 0, off_xc = 0;
@@ -625,7 +662,7 @@ int setup_p2p(exd_engine* h) {
   // buffers (exchange kernel). Halved per failed attempt down to a floor.
   const int64_t k_floor = std::max<int64_t>(1 << 20, 2 * h->cfg.k);
   int64_t xcap = h->cfg.n_g;
-  if (const char* pc = std::getenv("EXD_PUSH_CAP")) xcap = std::max<int64_t>(1, std::atoll(pc));
+  if (push_cap_env) xcap = std::max<int64_t>(1, std::atoll(push_cap_env));
   xcap = std::min<int64_t>(xcap, h->cfg.n_g);
   size_t spill_b = 0, sflag_b = 0, off_sp = 0, off_sf = 0;
   for (int attempt = 0; attempt < 64; ++attempt) {
@@ -758,10 +795,6 @@ int setup_p2p(exd_engine* h) {
         h->spill_flag_in[par] = reinterpret_cast<unsigned long long*>(own + off_sf + sflag_b * par);
       }
     }
-    // every rank must agree: the choice depends only on n (and the same
-    // environment on every rank)
-    h->holder_sum = n >= 4;
-    if (const char* hs = std::getenv("EXD_HOLDER_SUM")) h->holder_sum = hs[0] == '1';
   }
   std::vector<PeerFlags*> slot(n);
   std::vector<const int32_t*> lists(n);
@@ -789,13 +822,6 @@ int setup_p2p(exd_engine* h) {
   *h->p2p_err = 0;
   if (int r2 = alloc_zero((void**)&h->p2p_err_dev, sizeof(unsigned int))) return r2;
   if (int r2 = alloc_zero((void**)&h->p2p_gate, 3 * sizeof(unsigned long long))) return r2;
-  if (const char* tp = std::getenv("EXD_TWO_PASS")) h->two_pass = tp[0] == '1' ? 1 : 0;
-  if (const char* tk = std::getenv("EXD_TILE_PACK")) h->tile_pack = tk[0] == '1' ? 1 : 0;
-  {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-    h->xchg_blocks = 3 * sms - 1;
-  }
   if (h->xchg && h->tiles > kBaseRoundTiles)
     if (int r2 = alloc_zero((void**)&h->xrange_words, sizeof(unsigned long long) * 3 * kMaxCtas))
       return r2;

@@ -153,3 +153,12 @@ def test_two_ranks_baseline_sparsifiers_over_nccl(kind):
 def test_four_ranks_baseline_sparsifiers_over_nccl():
     _run(4, "--sparsifier", "topk", "--steps", "6", port=29613)
     _run(4, "--sparsifier", "cltk", "--steps", "6", "--dtype", "f64", port=29614)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("env", ["EXD_TILE_PACK=1", "EXD_HOLDER_SUM=1", "EXD_PUSH_CAP=5000"])
+def test_protocol_switches_must_agree_across_ranks(env):
+    # the peers' kernels read each other's inbox layout: a switch set on one
+    # rank only fails engine creation everywhere instead of corrupting the sum
+    _run(2, "--sync", "p2p", "--mismatch-env", env,
+         port=29620 + ["EXD_TILE_PACK=1", "EXD_HOLDER_SUM=1", "EXD_PUSH_CAP=5000"].index(env))

@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--inject", type=int, default=0,
                     help="perturb x on rank 1 after step 2; the next step must raise EngineError "
                          "(test_engine.cpp:219-226 across GPUs)")
+    ap.add_argument("--mismatch-env", default="",
+                    help="KEY=VAL set on rank 1 only before the engine is created; creation must "
+                         "fail on every rank with 'differs across ranks' instead of running two "
+                         "inbox protocols against each other")
     args = ap.parse_args()
 
     import numpy as np
@@ -57,6 +61,24 @@ def main():
     ids = [S.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     base = args.sparsifier != "exdyna"
+    if args.mismatch_env:
+        key, val = args.mismatch_env.split("=", 1)
+        if rank == 1:
+            os.environ[key] = val
+        msg = ""
+        try:
+            S.Engine.rank(S.SparsifierConfig(**kw), S.EngineOptions(dtype=args.dtype, sync=args.sync),
+                          rank, local, ids[0]).close()
+        except S.InvalidArgument as err:
+            msg = str(err)
+        good = "differs across ranks" in msg
+        flags = [None] * world
+        dist.all_gather_object(flags, (good, msg))
+        if rank == 0:
+            print(f"dist_check world={world} sync={args.sync} mismatch-env {args.mismatch_env}: "
+                  f"{'PASS' if all(f[0] for f in flags) else 'FAIL'} {flags}", flush=True)
+        dist.destroy_process_group()
+        sys.exit(0 if all(f[0] for f in flags) else 1)
     eng = S.Engine.rank(S.SparsifierConfig(**kw),
                         S.EngineOptions(dtype=args.dtype, sync=args.sync, sparsifier=args.sparsifier,
                                         fixed_delta=args.fixed if args.sparsifier == "hardthreshold" else 0.0),
