@@ -82,3 +82,37 @@ def test_errors_map_to_reference_exceptions():
     # engine construction validates before touching the device
     with pytest.raises(S.InvalidArgument, match="^n_b > n_g$"):
         S.Engine(S.SparsifierConfig(n=2, n_g=64, n_b=128, d=0.5, min_blk=1))
+
+
+def _resources():
+    """{mangled kernel name: {REG, STACK, SHARED, LOCAL}} from the sm_100a cubin."""
+    exe = "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--dump-resource-usage", LIB_PATH], capture_output=True,
+                         text=True).stdout
+    res, name = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+?):?$", line.strip())
+        if m:
+            name = m.group(1)
+            continue
+        if name and "REG:" in line:
+            res[name] = {k: int(v) for k, v in re.findall(r"(REG|STACK|SHARED|LOCAL):(\d+)", line)}
+            name = None
+    return res
+
+
+def test_hot_kernels_compiled_for_sm100a_without_local_memory():
+    # the stream kernel (K1) of the headline step (fp32, eta == 1, with and
+    # without the NVLink pushes) keeps everything in registers: no stack, no
+    # local memory, at most 64 registers (4 CTAs of 256 threads per SM)
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    res = _resources()
+    for push in ("0", "1"):
+        key = [k for k in res if f"stream_kernelIfLi0ELb1ELb{push}E" in k]
+        assert len(key) == 1, key
+        r = res[key[0]]
+        assert r["STACK"] == 0 and r["LOCAL"] == 0 and r["REG"] <= 64, (key[0], r)
